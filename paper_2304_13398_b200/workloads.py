@@ -1,0 +1,467 @@
+"""Seeded synthetic inputs: netlists, delays and stimuli.
+
+This module holds NO arithmetic of the simulation method (no gate function, no
+delay selection, no filtering).  It only draws random netlists and given
+waveforms with the shapes of the paper's workloads (Table 2),
+following the recipe in DESIGN.md §6.  It is shared by both sides of every
+parity check (the CUDA path and the oracle), which is allowed because it
+produces inputs only.
+
+Stimuli are COUNTER-BASED: the level of primary input i in epoch e is a pure
+function hash(seed, i, e), so any time window of any PI can be generated
+directly, on the CPU or on the GPU, with bit-identical results (int64 torch ops
+with wrapping multiply; tests check CPU == GPU).  Netlists and per-PI activity
+parameters are drawn on the host with numpy's PCG64.
+
+Value codes: 0, 1, X = 2, Z = 3.  Packed transition: (t << 2) | v.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+BUF, NOT, AND, NAND, OR, NOR, XOR, XNOR, MUX2 = range(9)
+TYPE_NAMES = ["BUF", "NOT", "AND", "NAND", "OR", "NOR", "XOR", "XNOR", "MUX2"]
+
+
+# --------------------------------------------------------------------------
+# data containers (plain arrays, the C-ABI layout)
+# --------------------------------------------------------------------------
+@dataclass
+class Netlist:
+    num_inputs: int
+    gate_type: np.ndarray      # uint8 [G]
+    fanin_offsets: np.ndarray  # int64 [G+1]
+    fanin_net: np.ndarray      # int32 [E]
+    pin_delay: np.ndarray      # uint32 [E, 4]  (rise->0, rise->1, fall->0, fall->1)
+    names: list | None = None  # optional net names (small circuits)
+
+    @property
+    def num_gates(self) -> int:
+        return int(self.gate_type.shape[0])
+
+    @property
+    def num_nets(self) -> int:
+        return self.num_inputs + self.num_gates
+
+    @property
+    def num_pins(self) -> int:
+        return int(self.fanin_net.shape[0])
+
+
+@dataclass
+class Stimuli:
+    offsets: np.ndarray   # int64 [P+1]
+    trans: np.ndarray     # uint64 [T]   packed (t << 2) | v
+
+    @property
+    def total(self) -> int:
+        return int(self.trans.shape[0])
+
+
+def pack(t, v) -> int:
+    return (int(t) << 2) | int(v)
+
+
+def stimuli_from_lists(waves) -> Stimuli:
+    """waves: list (per PI) of [(t, v), ...]."""
+    offs = np.zeros(len(waves) + 1, np.int64)
+    flat = []
+    for i, w in enumerate(waves):
+        offs[i + 1] = offs[i] + len(w)
+        flat.extend(pack(t, v) for t, v in w)
+    return Stimuli(offs, np.array(flat, dtype=np.uint64))
+
+
+def netlist_from_gates(num_inputs, gates, names=None) -> Netlist:
+    """gates: list of (type, [fanin nets], [(r0,r1,f0,f1) per pin])."""
+    G = len(gates)
+    offs = np.zeros(G + 1, np.int64)
+    nets, dl = [], []
+    types = np.zeros(G, np.uint8)
+    for g, (t, fin, d) in enumerate(gates):
+        types[g] = t
+        offs[g + 1] = offs[g] + len(fin)
+        nets.extend(fin)
+        dl.extend(d)
+    return Netlist(num_inputs, types, offs, np.array(nets, np.int32).reshape(-1),
+                   np.array(dl, np.uint32).reshape(-1, 4), names)
+
+
+# --------------------------------------------------------------------------
+# counter-based hashing (int64 torch ops, identical on CPU and GPU)
+# --------------------------------------------------------------------------
+def _i64(c: int) -> int:
+    return c - (1 << 64) if c >= (1 << 63) else c
+
+
+_K1 = _i64(0x9E3779B97F4A7C15)
+_K2 = _i64(0xBF58476D1CE4E5B9)
+_K3 = _i64(0x94D049BB133111EB)
+
+
+def _srl(x: torch.Tensor, k: int) -> torch.Tensor:
+    return (x >> k) & ((1 << (64 - k)) - 1)
+
+
+def _mix(x: torch.Tensor) -> torch.Tensor:
+    x = x + _K1
+    x = (x ^ _srl(x, 30)) * _K2
+    x = (x ^ _srl(x, 27)) * _K3
+    return x ^ _srl(x, 31)
+
+
+def _hash3(seed: int, a: torch.Tensor, b: torch.Tensor, tag: int) -> torch.Tensor:
+    """uniform 63-bit non-negative hash of (seed, a, b, tag)."""
+    x = _mix(torch.full_like(a, _i64((seed * 0x100000001B3 + tag * 0x9E37) & ((1 << 64) - 1))) ^ a)
+    x = _mix(x ^ (b * _K3))
+    return _srl(x, 1)
+
+
+# --------------------------------------------------------------------------
+# stimulus model: clocked, period 10,000 ps
+# --------------------------------------------------------------------------
+PERIOD = 10_000
+_TAG_OFF, _TAG_PHASE, _TAG_JIT, _TAG_LVL = 11, 12, 13, 14
+
+
+@dataclass
+class StimSpec:
+    """Clocked stimuli for `num_inputs` PIs over `ncycles` cycles.
+
+    PI i toggles only at epoch boundaries; epoch length L_i cycles (1 for the
+    "random" profile = the paper's 0.50 toggles/cycle designs, PAPER.md:527,529;
+    lognormal-distributed for the "skewed" profile to reach a target WCV,
+    Eq. 5).  In each epoch the level is 0/1 with 99 %
+    probability (0.5 % X, 0.5 % Z); a transition happens where the level differs
+    from the previous epoch's.  Times: cycle*PERIOD + offset_i + jitter(i,cycle)
+    with offset_i in [20,80] and jitter in [0,5].
+    """
+    seed: int
+    num_inputs: int
+    ncycles: int
+    epoch_len: np.ndarray = field(repr=False, default=None)  # int64 [P] (>=1)
+
+    @property
+    def duration(self) -> int:
+        # the paper's duration pattern: ncycles * 10^4 + 1 (e.g. 19,990,001 for 1,999 cycles)
+        return self.ncycles * PERIOD + 1
+
+
+def make_stimspec(seed, num_inputs, ncycles, profile="random", mean_trans=None, wcv=None) -> StimSpec:
+    if profile == "random":
+        L = np.ones(num_inputs, np.int64)
+    elif profile == "skewed":
+        assert mean_trans and wcv
+        rng = np.random.Generator(np.random.PCG64(seed + 7919))
+        sigma = math.sqrt(math.log(1.0 + wcv * wcv))
+        z = rng.standard_normal(num_inputs)
+        c = mean_trans * np.exp(sigma * z - 0.5 * sigma * sigma)
+        L = np.rint(0.5 * ncycles / np.maximum(c, 1e-9))
+        L = np.clip(L, 1, ncycles).astype(np.int64)
+    else:
+        raise ValueError(profile)
+    return StimSpec(seed, num_inputs, ncycles, L)
+
+
+def _pi_params(spec: StimSpec, pis: torch.Tensor):
+    dev = pis.device
+    L = torch.as_tensor(spec.epoch_len, device=dev)[pis]
+    off = 20 + _hash3(spec.seed, pis, torch.zeros_like(pis), _TAG_OFF) % 61
+    phase = _hash3(spec.seed, pis, torch.zeros_like(pis), _TAG_PHASE) % L
+    return L, off, phase
+
+
+def _level(spec: StimSpec, pis: torch.Tensor, epoch: torch.Tensor) -> torch.Tensor:
+    u = _hash3(spec.seed, pis, epoch, _TAG_LVL)
+    r = u % 1000
+    bit = (u >> 20) & 1
+    lvl = torch.where(r < 5, torch.full_like(u, 2), torch.where(r < 10, torch.full_like(u, 3), bit))
+    # the first epoch starts from the initial X: force a 0/1 level there
+    return torch.where(epoch == 0, bit, lvl)
+
+
+def _epoch_of_cycle(k, L, phase):
+    # epoch 0 = cycles [0, L - phase); epoch e>=1 starts at cycle e*L - phase
+    return torch.div(k + phase, L, rounding_mode="floor")
+
+
+def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
+                     cycle_lo: int = 0, cycle_hi: int | None = None):
+    """All transitions of every PI whose cycle lies in [cycle_lo, cycle_hi).
+
+    Returns (offsets int64 [P+1], trans int64-as-uint64 [T]) as torch tensors on
+    `device`.  With cycle_lo = 0 and cycle_hi = ncycles this is the whole
+    stimulus set.  Transition at cycle k of PI i exists iff k starts an epoch
+    (or k = 0) and level(epoch(k)) != level(epoch(k) - 1) (level(-1) = X).
+    """
+    dev = torch.device(device)
+    P = spec.num_inputs
+    if cycle_hi is None:
+        cycle_hi = spec.ncycles
+    counts = torch.zeros(P, dtype=torch.int64, device=dev)
+    chunks = []
+    for p0 in range(0, P, pi_batch):
+        pis = torch.arange(p0, min(P, p0 + pi_batch), device=dev, dtype=torch.int64)
+        L, off, phase = _pi_params(spec, pis)
+        e_lo = _epoch_of_cycle(torch.full_like(pis, cycle_lo), L, phase)
+        e_hi = _epoch_of_cycle(torch.full_like(pis, max(cycle_hi - 1, cycle_lo)), L, phase)
+        n_ep = torch.where(torch.full_like(pis, cycle_hi) > cycle_lo, e_hi - e_lo + 1, torch.zeros_like(pis))
+        tot = int(n_ep.sum().item())
+        if tot == 0:
+            continue
+        rep = torch.repeat_interleave(torch.arange(pis.numel(), device=dev), n_ep)
+        start = torch.cumsum(n_ep, 0) - n_ep
+        e = e_lo[rep] + (torch.arange(tot, device=dev, dtype=torch.int64) - start[rep])
+        pi = pis[rep]
+        Lr, phr, offr = L[rep], phase[rep], off[rep]
+        k = torch.clamp(e * Lr - phr, min=0)           # first cycle of the epoch
+        ok = (k >= cycle_lo) & (k < cycle_hi) & (k < spec.ncycles)
+        cur = _level(spec, pi, e)
+        prv = torch.where(e == 0, torch.full_like(e, 2), _level(spec, pi, torch.clamp(e - 1, min=0)))
+        m = ok & (cur != prv)
+        pi, k, cur, offr = pi[m], k[m], cur[m], offr[m]
+        jit = _hash3(spec.seed, pi, k, _TAG_JIT) % 6
+        t = k * PERIOD + offr + jit
+        chunks.append((t << 2) | cur)
+        counts[p0:p0 + pis.numel()] += torch.bincount(pi - p0, minlength=pis.numel())
+    offs = torch.zeros(P + 1, dtype=torch.int64, device=dev)
+    offs[1:] = torch.cumsum(counts, 0)
+    trans = torch.cat(chunks) if chunks else torch.zeros(0, dtype=torch.int64, device=dev)
+    return offs, trans
+
+
+def stimuli_window(spec: StimSpec, t_clamp: int, t_hi: int) -> Stimuli:
+    """Given waveforms restricted to a window, for oracle samples (CPU).
+
+    Every transition with t_clamp < t <= t_hi is kept; all transitions at or
+    before t_clamp are collapsed into one transition AT t_clamp carrying the
+    value in effect there (omitted if that value is the initial X).  With
+    t_clamp < 0 this is the plain prefix [0, t_hi].  The halo argument that
+    makes such windows exact is DESIGN.md §4 (reading R17)."""
+    P = spec.num_inputs
+    k_hi = min(spec.ncycles, t_hi // PERIOD + 1)
+    if t_clamp < 0:
+        offs, tr = generate_stimuli(spec, "cpu", cycle_lo=0, cycle_hi=k_hi)
+        tr = tr.numpy().astype(np.uint64)
+        t = (tr >> np.uint64(2)).astype(np.int64)
+        keep = t <= t_hi
+        pi_of = np.repeat(np.arange(P), np.diff(offs.numpy()))
+        tr, pi_of = tr[keep], pi_of[keep]
+        counts = np.bincount(pi_of, minlength=P)
+        o = np.zeros(P + 1, np.int64)
+        o[1:] = np.cumsum(counts)
+        return Stimuli(o, tr)
+    # value at t_clamp: the level of the epoch holding the last transition <= t_clamp.
+    # The epoch of cycle k(t_clamp) may start at a cycle whose (jittered) time is
+    # after t_clamp, so look one cycle back as well.
+    k_c = max(0, t_clamp // PERIOD)
+    k_lo = max(0, k_c - 1)
+    offs, tr = generate_stimuli(spec, "cpu", cycle_lo=k_lo, cycle_hi=k_hi)
+    tr = tr.numpy().astype(np.uint64)
+    pi_of = np.repeat(np.arange(P), np.diff(offs.numpy()))
+    t = (tr >> np.uint64(2)).astype(np.int64)
+    v = (tr & np.uint64(3)).astype(np.int64)
+    pis = torch.arange(P, dtype=torch.int64)
+    L, off, phase = _pi_params(spec, pis)
+    # level in effect just before cycle k_lo's possible transition = level(epoch(k_lo - 1))
+    if k_lo > 0:
+        e_prev = _epoch_of_cycle(torch.full_like(pis, k_lo - 1), L, phase)
+        base = _level(spec, pis, e_prev).numpy()
+    else:
+        base = np.full(P, 2, np.int64)
+    val = base.copy()
+    before = t <= t_clamp
+    # the last transition at or before t_clamp per PI sets the value
+    idx = np.nonzero(before)[0]
+    if idx.size:
+        # entries are grouped by PI and time-ordered: keep each PI's last one
+        last = np.ones(idx.size, bool)
+        last[:-1] = pi_of[idx[:-1]] != pi_of[idx[1:]]
+        idx = idx[last]
+        val[pi_of[idx]] = v[idx]
+    after = ~before & (t <= t_hi)
+    waves_pi = pi_of[after]
+    waves_tr = tr[after]
+    has_clamp = val != 2
+    n_clamp = has_clamp.astype(np.int64)
+    counts = np.bincount(waves_pi, minlength=P) + n_clamp
+    o = np.zeros(P + 1, np.int64)
+    o[1:] = np.cumsum(counts)
+    out = np.zeros(int(o[-1]), np.uint64)
+    cl = np.nonzero(has_clamp)[0]
+    out[o[cl]] = (np.uint64(t_clamp) << np.uint64(2)) | val[cl].astype(np.uint64)
+    # scatter the in-window transitions after the clamp entries
+    start = o[:-1] + n_clamp
+    rank = np.arange(waves_pi.shape[0]) - np.searchsorted(waves_pi, waves_pi, side="left")
+    out[start[waves_pi] + rank] = waves_tr
+    return Stimuli(o, out)
+
+
+# --------------------------------------------------------------------------
+# netlist recipe (after SURVEY §8(d))
+# --------------------------------------------------------------------------
+_TYPE_W = {AND: 2, NAND: 3, OR: 2, NOR: 3, MUX2: 1, BUF: 1, NOT: 1}
+
+
+def recipe_netlist(seed: int, num_gates: int, depth: int, num_inputs: int,
+                   p_inj: float = 0.25, geo_p: float = 0.7, xor_frac: float = 0.05,
+                   shuffle: bool = False) -> Netlist:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    G, D, P = num_gates, depth, num_inputs
+    lvl_size = np.full(D, G // D, np.int64)
+    lvl_size[: G % D] += 1
+    lvl_start = np.zeros(D + 1, np.int64)
+    lvl_start[1:] = np.cumsum(lvl_size)
+    level = np.repeat(np.arange(1, D + 1), lvl_size)            # level of each gate (1..D)
+
+    # gate types
+    tw = np.array([_TYPE_W[t] for t in sorted(_TYPE_W)], np.float64)
+    tl = np.array(sorted(_TYPE_W), np.int64)
+    types = tl[rng.choice(len(tl), size=G, p=tw / tw.sum())]
+    isx = rng.random(G) < xor_frac
+    types[isx] = np.where(rng.random(int(isx.sum())) < 0.5, XOR, XNOR)
+    ar = rng.choice(np.array([2, 3, 4]), size=G, p=[0.6, 0.2, 0.2])
+    arity = np.where((types == BUF) | (types == NOT), 1, np.where(types == MUX2, 3, ar))
+
+    offs = np.zeros(G + 1, np.int64)
+    offs[1:] = np.cumsum(arity)
+    E = int(offs[-1])
+    pin_gate = np.repeat(np.arange(G), arity)
+    pin_idx = np.arange(E) - offs[pin_gate]
+    pin_lvl = level[pin_gate]
+
+    def pick_from_level(lv):
+        """random net of level lv (0 = PIs) for each entry of array lv."""
+        out = np.empty(lv.shape[0], np.int64)
+        is_pi = lv <= 0
+        out[is_pi] = rng.integers(0, P, size=int(is_pi.sum()))
+        g = ~is_pi
+        lg = lv[g]
+        sz = lvl_size[lg - 1]
+        out[g] = P + lvl_start[lg - 1] + (rng.random(int(g.sum())) * sz).astype(np.int64)
+        return out
+
+    src_lvl = np.where(pin_idx == 0, pin_lvl - 1, 0)
+    extra = pin_idx > 0
+    inj = rng.random(E) < p_inj
+    back = rng.geometric(geo_p, size=E)
+    src_lvl = np.where(extra, np.where(inj, 0, np.maximum(pin_lvl - back, 0)), src_lvl)
+    fanin = pick_from_level(src_lvl).astype(np.int32)
+
+    # delays (ps): per gate base U[5,40]; per pin/value +U[0,6]; in-edge +0..3; rise/fall +-4
+    base = rng.integers(5, 41, size=G)[pin_gate]
+    pv = rng.integers(0, 7, size=(E, 2))
+    eo = rng.integers(0, 4, size=(E, 2))
+    asym = rng.integers(-4, 5, size=E)
+    d = np.empty((E, 4), np.int64)
+    for e_ in range(2):
+        for v_ in range(2):
+            d[:, e_ * 2 + v_] = base + pv[:, v_] + eo[:, e_] + (asym if v_ == 1 else 0)
+    d = np.maximum(d, 0).astype(np.uint32)
+
+    nl = Netlist(P, types.astype(np.uint8), offs, fanin, d)
+    if shuffle:
+        nl = shuffle_gates(nl, seed + 1)
+    return nl
+
+
+def shuffle_gates(nl: Netlist, seed: int) -> Netlist:
+    """Random permutation of the gate order (net ids remapped) — exercises levelisation."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    G, P = nl.num_gates, nl.num_inputs
+    perm = rng.permutation(G)                  # new gate j = old gate perm[j]
+    inv = np.empty(G, np.int64)
+    inv[perm] = np.arange(G)
+    ar = np.diff(nl.fanin_offsets)[perm]
+    offs = np.zeros(G + 1, np.int64)
+    offs[1:] = np.cumsum(ar)
+    idx = np.concatenate([np.arange(nl.fanin_offsets[g], nl.fanin_offsets[g + 1]) for g in perm]) \
+        if G else np.zeros(0, np.int64)
+    fin = nl.fanin_net[idx].astype(np.int64)
+    fin = np.where(fin >= P, P + inv[np.maximum(fin - P, 0)], fin)
+    return Netlist(P, nl.gate_type[perm], offs, fin.astype(np.int32), nl.pin_delay[idx])
+
+
+# --------------------------------------------------------------------------
+# small random designs for parity tests (SPEC-style random DAGs)
+# --------------------------------------------------------------------------
+def random_dag(seed, num_inputs, num_gates, max_delay=10, min_delay=0, types=None) -> Netlist:
+    rng = np.random.Generator(np.random.PCG64(seed))
+    P = num_inputs
+    types = list(range(9)) if types is None else list(types)
+    gates = []
+    for g in range(num_gates):
+        t = int(rng.choice(types))
+        k = 1 if t in (BUF, NOT) else (3 if t == MUX2 else int(rng.integers(2, 5)))
+        fin = [int(rng.integers(0, P + g)) for _ in range(k)]
+        d = [tuple(int(x) for x in rng.integers(min_delay, max_delay + 1, size=4)) for _ in range(k)]
+        gates.append((t, fin, d))
+    return shuffle_gates(netlist_from_gates(P, gates), seed + 3)
+
+
+def random_stimuli(seed, num_inputs, max_trans, tmax, xz=0.2, min_gap=1, max_gap=None) -> Stimuli:
+    """Random given waveforms: strictly increasing times in [0, tmax], no repeated value,
+    first value not X; X/Z share `xz`."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    waves = []
+    max_gap = max_gap or max(2, tmax // max(1, max_trans))
+    for _ in range(num_inputs):
+        n = int(rng.integers(0, max_trans + 1))
+        w, t, prev = [], int(rng.integers(0, max_gap + 1)), 2
+        for _ in range(n):
+            if t > tmax:
+                break
+            while True:
+                r = rng.random()
+                v = (2 if rng.random() < 0.5 else 3) if r < xz else int(rng.integers(0, 2))
+                if v != prev:
+                    break
+            w.append((t, v))
+            prev = v
+            t += int(rng.integers(min_gap, max_gap + 1))
+        waves.append(w)
+    return stimuli_from_lists(waves)
+
+
+# --------------------------------------------------------------------------
+# named configurations (BASELINE.json configs)
+# --------------------------------------------------------------------------
+def c17() -> tuple[Netlist, list]:
+    names = ["N1", "N2", "N3", "N6", "N7", "N10", "N11", "N16", "N19", "N22", "N23"]
+    ix = {n: i for i, n in enumerate(names)}
+    g = [("N10", "N1", "N3"), ("N11", "N3", "N6"), ("N16", "N2", "N11"),
+         ("N19", "N11", "N7"), ("N22", "N10", "N16"), ("N23", "N16", "N19")]
+    gates = [(NAND, [ix[a], ix[b]], [(1, 1, 1, 1)] * 2) for _, a, b in g]
+    return netlist_from_gates(5, gates, names), names
+
+
+CONFIGS = {
+    # name: (num_gates, depth, num_inputs, ncycles, profile, mean_trans, wcv)
+    "c7552": dict(num_gates=3512, depth=40, num_inputs=207, ncycles=1999, profile="random"),
+    "c3_1m": dict(num_gates=1 << 20, depth=200, num_inputs=104858, ncycles=19999, profile="random"),
+    "c4_10m": dict(num_gates=10 * (1 << 20), depth=250, num_inputs=1 << 20, ncycles=297203,
+                   profile="skewed", mean_trans=1000, wcv=17.0),
+    "c5_set": dict(num_gates=1 << 20, depth=200, num_inputs=104858, ncycles=1999, profile="random"),
+}
+
+
+def config_netlist(name: str, seed: int = 1) -> Netlist:
+    c = CONFIGS[name]
+    return recipe_netlist(seed, c["num_gates"], c["depth"], c["num_inputs"])
+
+
+def config_stimspec(name: str, seed: int = 1, ncycles: int | None = None) -> StimSpec:
+    c = CONFIGS[name]
+    return make_stimspec(seed, c["num_inputs"], ncycles or c["ncycles"], c["profile"],
+                         c.get("mean_trans"), c.get("wcv"))
+
+
+def wcv(lengths) -> float:
+    """Eq. 5: sigma / mean of the given waveforms' lengths
+    (population sigma)."""
+    x = np.asarray(lengths, np.float64)
+    return float(x.std() / x.mean()) if x.size and x.mean() > 0 else 0.0
