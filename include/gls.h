@@ -1,0 +1,203 @@
+/*
+ * gls.h — C ABI of the B200-native waveform-based, timing-aware, 4-value
+ * gate-level re-simulation library (libgls.so).  Method: arxiv 2304.13398,
+ * "Acceleration for Timing-Aware Gate-Level Logic Simulation with One-Pass GPU
+ * Parallelism".  Citations are PAPER.md line numbers (P:n) with the section /
+ * equation / algorithm; readings of points the paper leaves open are numbered
+ * R1..R17 in DESIGN.md §3-§4.
+ *
+ * Problem (§2.1): given a combinational netlist of basic gates, the
+ * delays of its pins and the waveforms of the given nets (primary inputs and
+ * register outputs cut into pseudo-primary inputs, P:87 footnote), compute the
+ * waveform of every gate output over [0, duration].  Values are 4-valued
+ * 0/1/X/Z (§2.2); Z at a gate input is read as X; gate
+ * outputs are never Z.  Delays are pin-to-pin per input edge and output value,
+ * the minimum over inputs changing together (§2.3), with inertial
+ * "glitch eaten" filtering (Eq. 1).
+ *
+ * Conventions for every function:
+ *   - returns int status: GLS_OK (0) or a negative GLS_E* code; never aborts or
+ *     throws.  gls_last_error() gives a message for the last failing call.
+ *   - on error the context is unchanged (no partial update), except that a
+ *     failing gls_simulate leaves no valid result (gls_get_* -> GLS_ESTATE).
+ *   - every input array is COPIED during the call (host pointers may be freed on
+ *     return; device pointers may be reused once the call returns, because the
+ *     copy is ordered on the context's stream and the call synchronises it).
+ *   - a context is not thread-safe; distinct contexts are independent.
+ *   - all device work is issued on the stream given to gls_create.
+ */
+#ifndef GLS_H
+#define GLS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+enum {
+    GLS_OK = 0,
+    GLS_EINVAL = -1,  /* malformed argument (type, arity, id, delay, time, value) */
+    GLS_ECYCLE = -2,  /* combinational loop: the netlist is not a DAG (P:87 fn)   */
+    GLS_ENOMEM = -3,  /* device memory / arena / chunk table too small; message
+                         names the size needed; the call may be retried after
+                         gls_set_config with larger limits                         */
+    GLS_ESTATE = -4,  /* call-order violation (e.g. simulate before load)         */
+    GLS_ERANGE = -5,  /* time > duration, duration >= 2^61, or an output buffer
+                         smaller than the result                                   */
+    GLS_ECUDA = -6    /* CUDA runtime error (message has the CUDA error string)   */
+};
+
+/* ---- values and packing (§2.1 "value and time"; §2.2) ------- */
+enum { GLS_V0 = 0, GLS_V1 = 1, GLS_VX = 2, GLS_VZ = 3 };
+/* A transition is one uint64: time in ps in bits 63..2, value code in bits 1..0.
+ * Time must be < 2^61.  (The paper stores int64 + int8 = 9 B.) */
+#define GLS_PACK(t, v) ((((uint64_t)(t)) << 2) | ((uint64_t)(v) & 3u))
+#define GLS_TIME(e) ((int64_t)((uint64_t)(e) >> 2))
+#define GLS_VAL(e) ((int)((e) & 3u))
+
+/* ---- basic gates (Table 1; composition §3.3) -------- */
+enum {
+    GLS_BUF = 0,  /* arity 1                                                   */
+    GLS_NOT = 1,  /* arity 1                                                   */
+    GLS_AND = 2,  /* arity 2..4, left fold of Table 1(a) (reading R10)         */
+    GLS_NAND = 3, /* NOT(AND)                                                  */
+    GLS_OR = 4,   /* arity 2..4, Table 1(b)                                    */
+    GLS_NOR = 5,  /* NOT(OR)                                                   */
+    GLS_XOR = 6,  /* arity 2..4, Table 1(c)                                    */
+    GLS_XNOR = 7, /* NOT(XOR)                                                  */
+    GLS_MUX2 = 8  /* arity 3, pins (a, b, sel): OR(AND(a,NOT sel),AND(b,sel)),
+                     reading R11                                              */
+};
+
+typedef struct gls_ctx gls_ctx;
+
+/* ---- tuning knobs (all optional; zero = default) ------------------------ */
+typedef struct gls_config {
+    int64_t arena_bytes;     /* transition store for given + computed waveforms
+                                (one store); 0 = auto (most of the
+                                free HBM)                     */
+    int64_t chunk_capacity;  /* max (gate, time-chunk) work items per run; 0 = auto */
+    int32_t chunk_events;    /* target merged input events per work item (M); 0 = 256 */
+    int32_t blocks_per_sm;   /* persistent-kernel CTAs per SM; 0 = max co-resident */
+    int32_t ring_limit;      /* TESTING: cap on the on-chip pending-schedule ring
+                                (1..32) to force the deep-backtrace path; 0 = 32 */
+    int32_t reserved[7];
+} gls_config;
+
+typedef struct gls_stats {
+    int64_t gate_evals;      /* Σ_g distinct fan-in timestamps (one calculateSignals
+                                of Alg. 2 each)                              */
+    int64_t events;          /* zero-delay output changes (Alg. 2 "o_k.v is changed") */
+    int64_t out_transitions; /* Σ_g |W(g)| after filtering and clipping            */
+    int64_t chunks;          /* (gate, time-chunk) work items processed            */
+    int64_t deep_chunks;     /* work items that needed the deep-backtrace path     */
+    int64_t levels;          /* topological levels (device barriers = 2 per level) */
+    int64_t arena_used_bytes;
+    int64_t alg_bytes;       /* algorithmic bytes of the gate-evaluation kernel
+                                (DESIGN.md §7): 8·Σ fan-in reads + 8·outputs +
+                                20·pins + 8·gates                                  */
+    double kernel_ms;        /* CUDA-event time of the gate-evaluation kernel      */
+    double simulate_ms;      /* CUDA-event time of the whole gls_simulate          */
+} gls_stats;
+
+/* ---- lifetime ----------------------------------------------------------- */
+/* Create a context on CUDA device `cuda_device`, issuing all work on
+ * `cuda_stream` (a cudaStream_t; NULL = the legacy default stream; a
+ * torch.cuda.Stream's .cuda_stream is accepted).  *out is NULL on error. */
+int gls_create(gls_ctx **out, int cuda_device, void *cuda_stream);
+/* Free all device and host memory of the context.  NULL is a no-op. */
+void gls_destroy(gls_ctx *ctx);
+/* Message of the last failing call on ctx ("" if none).  Owned by ctx. */
+const char *gls_last_error(const gls_ctx *ctx);
+/* Library version string (static storage). */
+const char *gls_version(void);
+/* Replace the tuning knobs (copied).  Takes effect at the next gls_simulate. */
+int gls_set_config(gls_ctx *ctx, const gls_config *cfg);
+
+/* ---- netlist (a1: validation + levelisation) -------------- */
+/* Nets: 0..num_inputs-1 are the given waveforms (primary / pseudo-primary
+ * inputs); num_inputs + g is the output of gate g (caller's gate order).
+ *   gate_type     [num_gates]        GLS_BUF..GLS_MUX2
+ *   fanin_offsets [num_gates+1]      CSR over pins, fanin_offsets[0] = 0; the
+ *                                    pin order is the gate function's operand order
+ *   fanin_net     [E]                driving net id of each pin, E = fanin_offsets[G]
+ *   pin_delay     [E][4]             ps, u32 < 2^31, per pin:
+ *                                    [0] in-edge RISE, output -> 0
+ *                                    [1] in-edge RISE, output -> 1
+ *                                    [2] in-edge FALL, output -> 0
+ *                                    [3] in-edge FALL, output -> 1
+ *                                    (the paper's 5-D matrix Delay[cell][in][out]
+ *                                    [edge][value], for single-output
+ *                                    gates; output -> X uses min of the two,
+ *                                    reading R1; an input edge is RISE iff the
+ *                                    value rises in the order 0 < X < 1, R2)
+ * Errors: GLS_EINVAL (type, arity, id out of range, delay >= 2^31, E >= 2^31,
+ * num_inputs + num_gates >= 2^31), GLS_ECYCLE (loop), GLS_ENOMEM, GLS_ECUDA.
+ * Loading replaces any previous netlist and clears the inputs and results. */
+int gls_load_netlist(gls_ctx *ctx, int32_t num_inputs, int32_t num_gates,
+                     const uint8_t *gate_type, const int64_t *fanin_offsets,
+                     const int32_t *fanin_net, const uint32_t *pin_delay);
+
+/* ---- given waveforms (a2) ------------------------------------------------ */
+/* CSR of packed transitions on the num_inputs given nets (HOST pointers):
+ *   offsets     [num_inputs+1], offsets[0] = 0, non-decreasing
+ *   transitions [offsets[num_inputs]] GLS_PACK(t, v)
+ * Per net: times strictly increasing, 0 <= t < 2^61; value codes 0..3; no
+ * value equal to the previous one, where the value before the first transition
+ * is X (so a first transition to X is rejected; Z is a distinct code) — the
+ * waveform rules of §2.1 and reading R6.  A net with no transition is
+ * constant X.  Errors: GLS_EINVAL, GLS_ESTATE (no netlist / num_inputs
+ * mismatch), GLS_ENOMEM, GLS_ECUDA.  May be repeated (re-simulation with a new
+ * stimulus set, the netlist stays loaded). */
+int gls_set_input_waveforms(gls_ctx *ctx, int32_t num_inputs, const int64_t *offsets,
+                            const uint64_t *transitions);
+/* Same, from DEVICE pointers on the context's device (validated on the device). */
+int gls_set_input_waveforms_device(gls_ctx *ctx, int32_t num_inputs, const int64_t *d_offsets,
+                                   const uint64_t *d_transitions, int64_t total);
+
+/* ---- simulation (a3-a9: one persistent-kernel pass, no host round trip) -- */
+/* Simulate every gate over [0, duration]; output transitions that would appear
+ * after `duration` are dropped (reading R7).  Errors: GLS_ESTATE (no netlist or
+ * inputs), GLS_ERANGE (a given transition later than duration, or duration <
+ * 0 or >= 2^61), GLS_ENOMEM (arena / chunk table too small: message gives the
+ * bytes needed; retry after gls_set_config), GLS_ECUDA.  Synchronous: returns
+ * when the result is on the device. */
+int gls_simulate(gls_ctx *ctx, int64_t duration);
+
+/* ---- results (a10) ------------------------------------------------------ */
+/* Canonical CSR of all num_inputs + num_gates nets, in net order (given nets
+ * verbatim, Z included).  Two-call protocol: with transitions == NULL only
+ * *total_out (and offsets if non-NULL) are written.  capacity = number of
+ * uint64 slots in `transitions`; GLS_ERANGE if smaller than the total.
+ * HOST pointers.  GLS_ESTATE if no successful simulation. */
+int gls_get_waveforms(gls_ctx *ctx, int64_t *offsets, uint64_t *transitions,
+                      int64_t capacity, int64_t *total_out);
+/* Per-net 64-bit hash, host array [num_inputs + num_gates], net order:
+ * h = splitmix64(0x9E3779B97F4A7C15 ^ n); h = splitmix64(h ^ e) for each of the
+ * net's n packed entries e.  Computed on the device. */
+int gls_get_net_hashes(gls_ctx *ctx, uint64_t *hashes);
+/* Same into a DEVICE array (for NCCL gathers). */
+int gls_get_net_hashes_device(gls_ctx *ctx, uint64_t *d_hashes);
+/* Per-net transition counts, host int64 [num_inputs + num_gates]. */
+int gls_get_net_counts(gls_ctx *ctx, int64_t *counts);
+/* Counters and timings of the last gls_simulate. */
+int gls_get_stats(gls_ctx *ctx, gls_stats *out);
+/* 1 + maximum path delay (Σ of max pin delays along the worst path): the halo
+ * that makes a time window exact (reading R17).  Needs a netlist. */
+int gls_get_halo(gls_ctx *ctx, int64_t *halo_ps);
+/* Number of topological levels of the loaded netlist (0 without gates). */
+int gls_get_levels(gls_ctx *ctx, int32_t *levels);
+
+/* ---- test hook ---------------------------------------------------------- */
+/* The library's own 4-value LUT entry for gate `type` with `arity` pins at
+ * input codes v[0..arity-1] (host-built table staged in shared memory by the
+ * kernel).  Returns the output code (0,1,2) or GLS_EINVAL. */
+int gls_lut_lookup(int type, int arity, const uint8_t *v);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLS_H */

@@ -1,0 +1,764 @@
+// gls_api.cu — host side of the C ABI declared in include/gls.h.
+//
+// a1 netlist validation + levelisation (Kahn order, counting sort by level,
+// fan-in CSR in level order), a2 given-waveform validation + packing into the
+// device store, the 4-value LUT build (a3), memory sizing, the single
+// persistent-kernel launch (a4-a9) and result readback (a10).  DESIGN.md §5.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/gls.h"
+#include "gls_internal.cuh"
+
+using namespace gls;
+
+namespace {
+
+// ---------------------------------------------------------------- 4-value LUT
+// Built from a dual-rail reading of X = "0 or 1": a value is the pair
+// (can_be_0, can_be_1); Z is read as X.  AND/OR/XOR on the pairs reproduce
+// Table 1; N-gates negate; MUX2 is composed as in reading R11.
+struct Dual { bool c0, c1; };
+Dual dual(int v) { return v == 0 ? Dual{true, false} : v == 1 ? Dual{false, true} : Dual{true, true}; }
+int undual(Dual d) { return d.c0 && d.c1 ? 2 : (d.c1 ? 1 : 0); }
+Dual d_not(Dual a) { return Dual{a.c1, a.c0}; }
+Dual d_and(Dual a, Dual b) { return Dual{a.c0 || b.c0, a.c1 && b.c1}; }
+Dual d_or(Dual a, Dual b) { return Dual{a.c0 && b.c0, a.c1 || b.c1}; }
+Dual d_xor(Dual a, Dual b) {
+    return Dual{(a.c0 && b.c0) || (a.c1 && b.c1), (a.c0 && b.c1) || (a.c1 && b.c0)};
+}
+
+int lut_eval(int type, int k, const int* v) {
+    if (k < 1 || k > 4) return -1;
+    Dual x[4] = {};
+    for (int i = 0; i < k && i < 4; ++i) x[i] = dual(v[i]);
+    Dual r;
+    switch (type) {
+        case GLS_BUF: r = x[0]; break;
+        case GLS_NOT: r = d_not(x[0]); break;
+        case GLS_AND: case GLS_NAND:
+            r = x[0];
+            for (int i = 1; i < k; ++i) r = d_and(r, x[i]);
+            if (type == GLS_NAND) r = d_not(r);
+            break;
+        case GLS_OR: case GLS_NOR:
+            r = x[0];
+            for (int i = 1; i < k; ++i) r = d_or(r, x[i]);
+            if (type == GLS_NOR) r = d_not(r);
+            break;
+        case GLS_XOR: case GLS_XNOR:
+            r = x[0];
+            for (int i = 1; i < k; ++i) r = d_xor(r, x[i]);
+            if (type == GLS_XNOR) r = d_not(r);
+            break;
+        case GLS_MUX2: r = d_or(d_and(x[0], d_not(x[2])), d_and(x[1], x[2])); break;
+        default: return -1;
+    }
+    return undual(r);
+}
+
+bool arity_ok(int type, int64_t k) {
+    if (type == GLS_BUF || type == GLS_NOT) return k == 1;
+    if (type == GLS_MUX2) return k == 3;
+    if (type >= GLS_AND && type <= GLS_XNOR) return k >= 2 && k <= 4;
+    return false;
+}
+
+const std::vector<uint8_t>& lut_table() {
+    static std::vector<uint8_t> t;
+    if (t.empty()) {
+        t.assign(kLutBytes, 2);
+        for (int type = 0; type < kNumTypes; ++type)
+            for (int k = 1; k <= 4; ++k) {
+                int base = lut_offset(type, k);
+                for (int idx = 0; idx < (1 << (2 * k)); ++idx) {
+                    int v[4];
+                    bool valid = true;
+                    for (int i = 0; i < k; ++i) {
+                        v[i] = (idx >> (2 * i)) & 3;
+                        if (v[i] == 3) valid = false;  // the kernel indexes normalised codes
+                    }
+                    if (!valid || !arity_ok(type, k)) continue;
+                    t[base + idx] = (uint8_t)lut_eval(type, k, v);
+                }
+            }
+    }
+    return t;
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t alloc(size_t count) {
+        release();
+        if (count == 0) count = 1;
+        cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+        if (e != cudaSuccess) { p = nullptr; n = 0; return e; }
+        n = count;
+        return cudaSuccess;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+}  // namespace
+
+struct gls_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    gls_config cfg{};
+    std::string err;
+
+    // netlist
+    bool has_netlist = false;
+    int32_t P = 0, G = 0, L = 0;
+    int64_t E = 0;
+    int64_t halo = 1;
+    std::vector<uint32_t> perm;        // internal gate -> user gate
+    std::vector<uint32_t> inv;         // user gate -> internal gate
+    std::vector<int64_t> net_fanout;   // internal net -> pins it drives
+    DevBuf<int32_t> d_level_off;
+    DevBuf<GateInfo> d_gate;
+    DevBuf<uint32_t> d_pin_src;
+    DevBuf<uint4> d_pin_delay;
+    DevBuf<uint8_t> d_lut;
+    DevBuf<uint32_t> d_perm;
+    DevBuf<uint32_t> d_net_ck, d_net_nck, d_gate_done;
+    DevBuf<unsigned long long> d_net_len;
+    DevBuf<unsigned long long> d_work;
+
+    // given waveforms (in the arena prefix)
+    bool has_inputs = false;
+    int64_t in_total = 0;
+    int64_t max_in_time = -1;
+    DevBuf<long long> d_in_off;
+    DevBuf<uint64_t> d_arena;
+    bool arena_auto = true;
+
+    // chunk tables
+    DevBuf<long long> d_ck_T;
+    DevBuf<unsigned long long> d_ck_off, d_ck_cum;
+    DevBuf<uint32_t> d_ck_cnt, d_ck_gate;
+    DevBuf<uint8_t> d_ck_vb;
+    DevBuf<uint64_t> d_deep;
+    DevBuf<Ctl> d_ctl;
+    DevBuf<unsigned> d_flag;
+    DevBuf<unsigned long long> d_flag64;
+
+    // results
+    bool has_result = false;
+    int64_t duration = 0;
+    Ctl last{};
+    gls_stats stats{};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+int fail(gls_ctx* c, int code, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    if (c) c->err = buf;
+    return code;
+}
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess) {                                                                   \
+            cudaGetLastError();                                                                    \
+            return fail(ctx, e_ == cudaErrorMemoryAllocation ? GLS_ENOMEM : GLS_ECUDA,             \
+                        "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__);      \
+        }                                                                                          \
+    } while (0)
+
+int64_t free_bytes(gls_ctx* ctx) {
+    size_t fr = 0, tot = 0;
+    cudaSetDevice(ctx->device);
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
+    return (int64_t)fr;
+}
+
+SimParams params(gls_ctx* ctx) {
+    SimParams p{};
+    p.P = ctx->P;
+    p.G = ctx->G;
+    p.L = ctx->L;
+    p.level_off = ctx->d_level_off.p;
+    p.gate = ctx->d_gate.p;
+    p.pin_src = ctx->d_pin_src.p;
+    p.pin_delay = ctx->d_pin_delay.p;
+    p.lut = ctx->d_lut.p;
+    p.arena = ctx->d_arena.p;
+    p.arena_cap = ctx->d_arena.n;
+    p.net_ck = ctx->d_net_ck.p;
+    p.net_nck = ctx->d_net_nck.p;
+    p.net_len = ctx->d_net_len.p;
+    p.ck_T = ctx->d_ck_T.p;
+    p.ck_off = ctx->d_ck_off.p;
+    p.ck_cnt = ctx->d_ck_cnt.p;
+    p.ck_cum = ctx->d_ck_cum.p;
+    p.ck_vb = ctx->d_ck_vb.p;
+    p.ck_gate = ctx->d_ck_gate.p;
+    p.ck_cap = ctx->d_ck_T.n;
+    p.gate_done = ctx->d_gate_done.p;
+    p.work = ctx->d_work.p;
+    p.deep = ctx->d_deep.p;
+    p.deep_cap = ctx->d_deep.n;
+    p.ctl = ctx->d_ctl.p;
+    p.duration = ctx->duration;
+    p.M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : 256;
+    int rl = ctx->cfg.ring_limit;
+    p.ring_cap = (rl > 0 && rl < kRing) ? rl : kRing;
+    return p;
+}
+
+// Chunk-table entries per arena entry for auto sizing.
+double chunk_ratio(gls_ctx* ctx) {
+    int M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : 256;
+    double fan = (double)ctx->E / std::max<double>(1.0, (double)ctx->P + ctx->G);
+    return 1.5 * (fan + 0.5) / (double)M;
+}
+
+constexpr int64_t kChunkBytes = 8 + 8 + 8 + 4 + 4 + 1;  // T, off, cum, cnt, gate, vb
+
+// (Re)allocate the arena so that it holds at least `min_entries`; keeps the
+// given-waveform prefix.  Auto mode sizes it from an output estimate, capped
+// by the free HBM.
+int ensure_arena(gls_ctx* ctx, int64_t min_entries, bool grow_max) {
+    int64_t want;
+    if (ctx->cfg.arena_bytes > 0) {
+        want = ctx->cfg.arena_bytes / 8;
+        ctx->arena_auto = false;
+    } else {
+        ctx->arena_auto = true;
+        int64_t per_pi = ctx->P ? std::max<int64_t>(16, ctx->in_total / ctx->P) : 16;
+        double est = (double)ctx->in_total + 3.0 * (double)ctx->G * (double)per_pi + 4096.0;
+        want = (int64_t)std::min(est, 4e18);
+        want = std::max<int64_t>(want, (256ll << 20) / 8);
+        int64_t have = (int64_t)ctx->d_arena.n;
+        int64_t avail = free_bytes(ctx) + have * 8;
+        double per_entry = 8.0 + kChunkBytes * chunk_ratio(ctx);
+        int64_t reserve = ((int64_t)ctx->G + ctx->P) * 24 + (256ll << 20);
+        int64_t cap = (int64_t)(std::max<int64_t>(0, (int64_t)(avail * 0.90) - reserve) / per_entry);
+        if (grow_max || want > cap) want = cap;
+    }
+    if (want < min_entries) want = min_entries;
+    if ((int64_t)ctx->d_arena.n >= want && !grow_max) return GLS_OK;
+    if ((int64_t)ctx->d_arena.n == want) return GLS_OK;
+    uint64_t* np = nullptr;
+    cudaError_t e = cudaMalloc(&np, (size_t)std::max<int64_t>(want, 1) * 8);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, GLS_ENOMEM, "arena allocation of %lld bytes failed: %s", (long long)want * 8,
+                    cudaGetErrorString(e));
+    }
+    if (ctx->d_arena.p && ctx->has_inputs && ctx->in_total > 0) {
+        e = cudaMemcpyAsync(np, ctx->d_arena.p, (size_t)ctx->in_total * 8, cudaMemcpyDeviceToDevice,
+                            ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) {
+            cudaFree(np);
+            return fail(ctx, GLS_ECUDA, "arena copy: %s", cudaGetErrorString(e));
+        }
+    }
+    ctx->d_arena.release();
+    ctx->d_arena.p = np;
+    ctx->d_arena.n = (size_t)std::max<int64_t>(want, 1);
+    return GLS_OK;
+}
+
+int ensure_chunks(gls_ctx* ctx, int64_t min_cap) {
+    int64_t want;
+    if (ctx->cfg.chunk_capacity > 0) {
+        want = ctx->cfg.chunk_capacity;
+    } else {
+        want = (int64_t)ctx->P + 2ll * ctx->G + (int64_t)(chunk_ratio(ctx) * (double)ctx->d_arena.n) + 1024;
+    }
+    want = std::max(want, min_cap);
+    want = std::max<int64_t>(want, (int64_t)ctx->P + ctx->G + 1);
+    if (want >= (1ll << 32)) want = (1ll << 32) - 1;
+    if ((int64_t)ctx->d_ck_T.n >= want) return GLS_OK;
+    cudaError_t e;
+    if ((e = ctx->d_ck_T.alloc(want)) != cudaSuccess || (e = ctx->d_ck_off.alloc(want)) != cudaSuccess ||
+        (e = ctx->d_ck_cum.alloc(want)) != cudaSuccess || (e = ctx->d_ck_cnt.alloc(want)) != cudaSuccess ||
+        (e = ctx->d_ck_gate.alloc(want)) != cudaSuccess || (e = ctx->d_ck_vb.alloc(want)) != cudaSuccess) {
+        cudaGetLastError();
+        ctx->d_ck_T.release();
+        return fail(ctx, GLS_ENOMEM, "chunk table of %lld entries: %s", (long long)want, cudaGetErrorString(e));
+    }
+    return GLS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* gls_version(void) { return "gls 0.1 (sm_100a, persistent level-barrier kernel)"; }
+
+const char* gls_last_error(const gls_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int gls_lut_lookup(int type, int arity, const uint8_t* v) {
+    if (type < 0 || type >= kNumTypes || !arity_ok(type, arity) || !v) return GLS_EINVAL;
+    int idx = 0;
+    for (int i = 0; i < arity; ++i) {
+        if (v[i] > 3) return GLS_EINVAL;
+        int c = v[i] == 3 ? 2 : v[i];  // Z read as X
+        idx |= c << (2 * i);
+    }
+    return lut_table()[lut_offset(type, arity) + idx];
+}
+
+int gls_create(gls_ctx** out, int cuda_device, void* cuda_stream) {
+    if (!out) return GLS_EINVAL;
+    *out = nullptr;
+    gls_ctx* ctx = new (std::nothrow) gls_ctx();
+    if (!ctx) return GLS_ENOMEM;
+    ctx->device = cuda_device;
+    ctx->stream = (cudaStream_t)cuda_stream;
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e == cudaSuccess) {
+        for (auto& ev : ctx->ev)
+            if (e == cudaSuccess) e = cudaEventCreate(&ev);
+    }
+    if (e == cudaSuccess) e = ctx->d_ctl.alloc(1);
+    if (e == cudaSuccess) e = ctx->d_flag.alloc(4);
+    if (e == cudaSuccess) e = ctx->d_flag64.alloc(4);
+    if (e == cudaSuccess) e = ctx->d_lut.alloc(kLutBytes);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(ctx->d_lut.p, lut_table().data(), kLutBytes, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete ctx;
+        return e == cudaErrorMemoryAllocation ? GLS_ENOMEM : GLS_ECUDA;
+    }
+    *out = ctx;
+    return GLS_OK;
+}
+
+void gls_destroy(gls_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    for (auto& ev : ctx->ev)
+        if (ev) cudaEventDestroy(ev);
+    delete ctx;
+}
+
+int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
+    if (!ctx || !cfg) return GLS_EINVAL;
+    if (cfg->arena_bytes < 0 || cfg->chunk_capacity < 0 || cfg->chunk_events < 0 || cfg->blocks_per_sm < 0 ||
+        cfg->ring_limit < 0 || cfg->ring_limit > kRing)
+        return fail(ctx, GLS_EINVAL, "invalid gls_config field");
+    ctx->cfg = *cfg;
+    return GLS_OK;
+}
+
+int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, const int64_t* off,
+                     const int32_t* net, const uint32_t* delay) {
+    if (!ctx) return GLS_EINVAL;
+    if (P < 0 || G < 0 || (int64_t)P + G >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "bad net counts");
+    if (G > 0 && (!type || !off)) return fail(ctx, GLS_EINVAL, "null netlist array");
+    const int64_t N = (int64_t)P + G;
+    const int64_t E = G > 0 ? off[G] : 0;
+    if (G > 0 && off[0] != 0) return fail(ctx, GLS_EINVAL, "fanin_offsets[0] != 0");
+    if (E < 0 || E >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "pin count out of range");
+    if (E > 0 && (!net || !delay)) return fail(ctx, GLS_EINVAL, "null pin array");
+    for (int32_t g = 0; g < G; ++g) {
+        int64_t k = off[g + 1] - off[g];
+        if (type[g] >= kNumTypes) return fail(ctx, GLS_EINVAL, "gate %d: unknown type %d", g, (int)type[g]);
+        if (!arity_ok(type[g], k)) return fail(ctx, GLS_EINVAL, "gate %d: arity %lld invalid", g, (long long)k);
+        for (int64_t e = off[g]; e < off[g + 1]; ++e) {
+            if (net[e] < 0 || net[e] >= N) return fail(ctx, GLS_EINVAL, "gate %d: net id %d out of range", g, net[e]);
+            for (int q = 0; q < 4; ++q)
+                if (delay[4 * e + q] >= (1u << 31)) return fail(ctx, GLS_EINVAL, "pin %lld: delay >= 2^31", (long long)e);
+        }
+    }
+    // Kahn topological order; level(g) = 1 + max level of driving gates (PIs at 0)
+    std::vector<int32_t> indeg(G, 0), level(G, 0), order;
+    std::vector<int64_t> fo_off((size_t)G + 1, 0);
+    for (int32_t g = 0; g < G; ++g)
+        for (int64_t e = off[g]; e < off[g + 1]; ++e)
+            if (net[e] >= P) { ++indeg[g]; ++fo_off[net[e] - P + 1]; }
+    for (int32_t g = 0; g < G; ++g) fo_off[g + 1] += fo_off[g];
+    std::vector<int32_t> fo((size_t)std::max<int64_t>(fo_off[G], 1));
+    {
+        std::vector<int64_t> fill(fo_off.begin(), fo_off.end() - 1);
+        for (int32_t g = 0; g < G; ++g)
+            for (int64_t e = off[g]; e < off[g + 1]; ++e)
+                if (net[e] >= P) fo[fill[net[e] - P]++] = g;
+    }
+    order.reserve(G);
+    for (int32_t g = 0; g < G; ++g)
+        if (indeg[g] == 0) order.push_back(g);
+    for (size_t h = 0; h < order.size(); ++h) {
+        int32_t g = order[h];
+        for (int64_t q = fo_off[g]; q < fo_off[g + 1]; ++q) {
+            int32_t c = fo[q];
+            level[c] = std::max(level[c], level[g] + 1);
+            if (--indeg[c] == 0) order.push_back(c);
+        }
+    }
+    if ((int64_t)order.size() != G) return fail(ctx, GLS_ECYCLE, "combinational loop: %lld gates on cycles",
+                                               (long long)(G - (int64_t)order.size()));
+    int32_t L = 0;
+    for (int32_t g = 0; g < G; ++g) { level[g] += 1; L = std::max(L, level[g]); }
+    // stable counting sort by level -> internal order
+    std::vector<int32_t> level_off((size_t)L + 1, 0);
+    for (int32_t g = 0; g < G; ++g) ++level_off[level[g]];
+    for (int32_t l = 1; l <= L; ++l) level_off[l] += level_off[l - 1];
+    std::vector<uint32_t> perm(G), inv(G);
+    {
+        std::vector<int32_t> fill(level_off.begin(), level_off.end() - 1);
+        for (int32_t g = 0; g < G; ++g) {
+            int32_t i = fill[level[g] - 1]++;
+            perm[i] = (uint32_t)g;
+            inv[g] = (uint32_t)i;
+        }
+    }
+    std::vector<GateInfo> ginfo(G);
+    std::vector<uint32_t> psrc((size_t)E);
+    std::vector<uint4> pdel((size_t)E);
+    std::vector<int64_t> fanout((size_t)N, 0);
+    std::vector<int64_t> arrive((size_t)N, 0);
+    int64_t maxA = 0;
+    uint32_t pin = 0;
+    for (int32_t i = 0; i < G; ++i) {
+        int32_t g = (int32_t)perm[i];
+        int k = (int)(off[g + 1] - off[g]);
+        ginfo[i].pin_off = pin;
+        ginfo[i].k = (uint8_t)k;
+        ginfo[i].lut_base = (uint16_t)lut_offset(type[g], k);
+        ginfo[i].pad = 0;
+        uint32_t dmax = 0;
+        int64_t a = 0;
+        for (int q = 0; q < k; ++q) {
+            int64_t e = off[g] + q;
+            int32_t s = net[e];
+            uint32_t si = s < P ? (uint32_t)s : (uint32_t)(P + inv[s - P]);
+            psrc[pin] = si;
+            pdel[pin] = make_uint4(delay[4 * e], delay[4 * e + 1], delay[4 * e + 2], delay[4 * e + 3]);
+            dmax = std::max({dmax, delay[4 * e], delay[4 * e + 1], delay[4 * e + 2], delay[4 * e + 3]});
+            ++fanout[si];
+            a = std::max(a, arrive[si]);
+            ++pin;
+        }
+        arrive[P + i] = a + dmax;
+        maxA = std::max(maxA, arrive[P + i]);
+    }
+    // upload
+    cudaSetDevice(ctx->device);
+    ctx->has_netlist = ctx->has_inputs = ctx->has_result = false;
+    CK(ctx->d_level_off.alloc(L + 1));
+    CK(ctx->d_gate.alloc(G));
+    CK(ctx->d_pin_src.alloc(E));
+    CK(ctx->d_pin_delay.alloc(E));
+    CK(ctx->d_perm.alloc(G));
+    CK(ctx->d_net_ck.alloc(N));
+    CK(ctx->d_net_nck.alloc(N));
+    CK(ctx->d_net_len.alloc(N));
+    CK(ctx->d_gate_done.alloc(G));
+    CK(ctx->d_work.alloc(L + 1));
+    CK(cudaMemcpy(ctx->d_level_off.p, level_off.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice));
+    if (G) {
+        CK(cudaMemcpy(ctx->d_gate.p, ginfo.data(), sizeof(GateInfo) * G, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_perm.p, perm.data(), sizeof(uint32_t) * G, cudaMemcpyHostToDevice));
+    }
+    if (E) {
+        CK(cudaMemcpy(ctx->d_pin_src.p, psrc.data(), sizeof(uint32_t) * E, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_pin_delay.p, pdel.data(), sizeof(uint4) * E, cudaMemcpyHostToDevice));
+    }
+    ctx->P = P;
+    ctx->G = G;
+    ctx->L = L;
+    ctx->E = E;
+    ctx->halo = maxA + 1;
+    ctx->perm.swap(perm);
+    ctx->inv.swap(inv);
+    ctx->net_fanout.swap(fanout);
+    ctx->has_netlist = true;
+    return GLS_OK;
+}
+
+static int set_inputs_common(gls_ctx* ctx, int32_t P, int64_t total) {
+    if (!ctx->has_netlist) return fail(ctx, GLS_ESTATE, "gls_set_input_waveforms before gls_load_netlist");
+    if (P != ctx->P) return fail(ctx, GLS_ESTATE, "num_inputs %d != netlist's %d", P, ctx->P);
+    if (total < 0) return fail(ctx, GLS_EINVAL, "negative total");
+    return GLS_OK;
+}
+
+int gls_set_input_waveforms(gls_ctx* ctx, int32_t P, const int64_t* offsets, const uint64_t* tr) {
+    if (!ctx) return GLS_EINVAL;
+    if (!offsets) return fail(ctx, GLS_EINVAL, "null offsets");
+    int rc = set_inputs_common(ctx, P, 0);
+    if (rc) return rc;
+    const int64_t total = offsets[P];
+    if (total < 0) return fail(ctx, GLS_EINVAL, "negative total");
+    if (offsets[0] != 0) return fail(ctx, GLS_EINVAL, "offsets[0] != 0");
+    if (total > 0 && !tr) return fail(ctx, GLS_EINVAL, "null transitions");
+    int64_t maxt = -1;
+    for (int32_t i = 0; i < P; ++i) {
+        if (offsets[i + 1] < offsets[i]) return fail(ctx, GLS_EINVAL, "offsets decrease at net %d", i);
+        int prev = GLS_VX;
+        int64_t pt = -1;
+        for (int64_t j = offsets[i]; j < offsets[i + 1]; ++j) {
+            int64_t t = GLS_TIME(tr[j]);
+            int v = GLS_VAL(tr[j]);
+            if (t >= (1ll << 61)) return fail(ctx, GLS_EINVAL, "net %d: time >= 2^61", i);
+            if (t <= pt) return fail(ctx, GLS_EINVAL, "net %d: times not strictly increasing at entry %lld", i, (long long)j);
+            if (v == prev) return fail(ctx, GLS_EINVAL, "net %d: value repeats the previous one at entry %lld", i, (long long)j);
+            prev = v;
+            pt = t;
+        }
+        maxt = std::max(maxt, pt);
+    }
+    ctx->has_inputs = ctx->has_result = false;
+    ctx->in_total = total;
+    rc = ensure_arena(ctx, total + 1, false);
+    if (rc) return rc;
+    CK(ctx->d_in_off.alloc(P + 1));
+    CK(cudaMemcpyAsync(ctx->d_in_off.p, offsets, sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, ctx->stream));
+    if (total)
+        CK(cudaMemcpyAsync(ctx->d_arena.p, tr, sizeof(uint64_t) * total, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->max_in_time = maxt;
+    ctx->has_inputs = true;
+    return GLS_OK;
+}
+
+int gls_set_input_waveforms_device(gls_ctx* ctx, int32_t P, const int64_t* d_off, const uint64_t* d_tr,
+                                   int64_t total) {
+    if (!ctx) return GLS_EINVAL;
+    int rc = set_inputs_common(ctx, P, total);
+    if (rc) return rc;
+    if (!d_off || (total > 0 && !d_tr)) return fail(ctx, GLS_EINVAL, "null device pointer");
+    ctx->has_inputs = ctx->has_result = false;
+    ctx->in_total = total;
+    rc = ensure_arena(ctx, total + 1, false);
+    if (rc) return rc;
+    CK(ctx->d_in_off.alloc(P + 1));
+    CK(cudaMemcpyAsync(ctx->d_in_off.p, d_off, sizeof(int64_t) * (P + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+    if (total)
+        CK(cudaMemcpyAsync(ctx->d_arena.p, d_tr, sizeof(uint64_t) * total, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_flag.p, 0, sizeof(unsigned) * 4, ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_flag64.p, 0, sizeof(unsigned long long) * 4, ctx->stream));
+    CK(launch_validate_inputs(P, ctx->d_in_off.p, ctx->d_arena.p, total, ctx->d_flag.p, ctx->d_flag64.p, ctx->stream));
+    unsigned err = 0;
+    unsigned long long mt = 0;
+    long long last_off = 0;
+    CK(cudaMemcpyAsync(&err, ctx->d_flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&mt, ctx->d_flag64.p, sizeof(mt), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&last_off, ctx->d_in_off.p + P, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (err || last_off != total)
+        return fail(ctx, GLS_EINVAL, "device given waveforms invalid (flags %u, offsets[P]=%lld, total=%lld)", err,
+                    last_off, (long long)total);
+    ctx->max_in_time = total ? (int64_t)mt : -1;
+    ctx->has_inputs = true;
+    return GLS_OK;
+}
+
+int gls_simulate(gls_ctx* ctx, int64_t duration) {
+    if (!ctx) return GLS_EINVAL;
+    if (!ctx->has_netlist) return fail(ctx, GLS_ESTATE, "gls_simulate before gls_load_netlist");
+    if (!ctx->has_inputs) return fail(ctx, GLS_ESTATE, "gls_simulate before gls_set_input_waveforms");
+    if (duration < 0 || duration >= (1ll << 61)) return fail(ctx, GLS_ERANGE, "duration out of range");
+    if (ctx->max_in_time > duration)
+        return fail(ctx, GLS_ERANGE, "a given transition at %lld ps is later than the duration %lld ps",
+                    (long long)ctx->max_in_time, (long long)duration);
+    cudaSetDevice(ctx->device);
+    ctx->has_result = false;
+    ctx->duration = duration;
+    int rc = ensure_chunks(ctx, 0);
+    if (rc) return rc;
+    if (!ctx->d_deep.p) CK(ctx->d_deep.alloc(std::max<int64_t>(1 << 20, std::min<int64_t>(16ll << 20, ctx->in_total))));
+    int per_sm = 0;
+    int maxb = max_coresident_blocks(ctx->device, &per_sm);
+    int sms = per_sm ? maxb / per_sm : 0;
+    int blocks = ctx->cfg.blocks_per_sm > 0 ? std::min(maxb, ctx->cfg.blocks_per_sm * sms) : maxb;
+    if (blocks < 1) return fail(ctx, GLS_ECUDA, "simulation kernel cannot be resident (occupancy 0)");
+
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        SimParams p = params(ctx);
+        Ctl init{};
+        init.chunk_top = (unsigned long long)ctx->P;
+        init.arena_top = (unsigned long long)ctx->in_total;
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        CK(cudaMemcpyAsync(ctx->d_ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemsetAsync(ctx->d_work.p, 0, sizeof(unsigned long long) * (ctx->L + 1), ctx->stream));
+        CK(launch_init_given(p, ctx->d_in_off.p, ctx->stream));
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (ctx->G > 0) CK(launch_simulate(p, blocks, ctx->stream));
+        CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+        CK(cudaMemcpyAsync(&ctx->last, ctx->d_ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        const Ctl& c = ctx->last;
+        if (c.error & kErrBug) return fail(ctx, GLS_ECUDA, "internal consistency check failed (pass counts differ)");
+        if (c.error & (kErrArena | kErrChunks | kErrDeep)) {
+            // grow what overflowed and retry (auto sizing), else report what is needed
+            bool retried = false;
+            if ((c.error & kErrDeep)) {
+                int64_t need = (int64_t)c.need_deep * 2;
+                CK(ctx->d_deep.alloc(need));
+                retried = true;
+            }
+            if ((c.error & kErrChunks)) {
+                if (ctx->cfg.chunk_capacity > 0)
+                    return fail(ctx, GLS_ENOMEM, "chunk table too small: %llu entries needed at the failing level (capacity %zu)",
+                                c.need_chunks, ctx->d_ck_T.n);
+                ctx->d_ck_T.release();
+                rc = ensure_chunks(ctx, (int64_t)(c.need_chunks * 2));
+                if (rc) return rc;
+                retried = true;
+            }
+            if ((c.error & kErrArena)) {
+                if (!ctx->arena_auto || attempt > 0)
+                    return fail(ctx, GLS_ENOMEM,
+                                "arena too small: more than %llu bytes needed (arena %zu bytes); set gls_config.arena_bytes",
+                                c.need_arena * 8ull, ctx->d_arena.n * 8);
+                rc = ensure_arena(ctx, (int64_t)c.need_arena, true);
+                if (rc) return rc;
+                ctx->d_ck_T.release();
+                rc = ensure_chunks(ctx, 0);
+                if (rc) return rc;
+                retried = true;
+            }
+            if (retried) continue;
+        }
+        // success
+        float ms_k = 0, ms_s = 0;
+        cudaEventElapsedTime(&ms_k, ctx->ev[1], ctx->ev[2]);
+        cudaEventElapsedTime(&ms_s, ctx->ev[0], ctx->ev[2]);
+        gls_stats& s = ctx->stats;
+        s = gls_stats{};
+        s.gate_evals = (int64_t)c.gate_evals;
+        s.events = (int64_t)c.events;
+        s.out_transitions = (int64_t)c.out_trans;
+        s.chunks = (int64_t)c.chunks;
+        s.deep_chunks = (int64_t)c.deep_chunks;
+        s.levels = ctx->L;
+        s.arena_used_bytes = (int64_t)c.arena_top * 8;
+        s.kernel_ms = ms_k;
+        s.simulate_ms = ms_s;
+        // algorithmic bytes: every fan-in waveform read once per pin
+        std::vector<unsigned long long> len((size_t)ctx->P + ctx->G);
+        if (!len.empty())
+            CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * len.size(), cudaMemcpyDeviceToHost));
+        long double reads = 0;
+        for (size_t n = 0; n < len.size(); ++n) reads += (long double)len[n] * (long double)ctx->net_fanout[n];
+        s.alg_bytes = (int64_t)(8.0L * reads + 8.0L * (long double)c.out_trans + 20.0L * ctx->E + 8.0L * ctx->G);
+        ctx->has_result = true;
+        return GLS_OK;
+    }
+    return fail(ctx, GLS_ENOMEM, "simulation did not fit after resizing");
+}
+
+int gls_get_stats(gls_ctx* ctx, gls_stats* out) {
+    if (!ctx || !out) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    *out = ctx->stats;
+    return GLS_OK;
+}
+
+int gls_get_halo(gls_ctx* ctx, int64_t* halo) {
+    if (!ctx || !halo) return GLS_EINVAL;
+    if (!ctx->has_netlist) return fail(ctx, GLS_ESTATE, "no netlist");
+    *halo = ctx->halo;
+    return GLS_OK;
+}
+
+int gls_get_levels(gls_ctx* ctx, int32_t* levels) {
+    if (!ctx || !levels) return GLS_EINVAL;
+    if (!ctx->has_netlist) return fail(ctx, GLS_ESTATE, "no netlist");
+    *levels = ctx->L;
+    return GLS_OK;
+}
+
+int gls_get_net_counts(gls_ctx* ctx, int64_t* counts) {
+    if (!ctx || !counts) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    const int64_t N = (int64_t)ctx->P + ctx->G;
+    std::vector<unsigned long long> len((size_t)N);
+    if (N) CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost));
+    for (int32_t i = 0; i < ctx->P; ++i) counts[i] = (int64_t)len[i];
+    for (int32_t g = 0; g < ctx->G; ++g) counts[ctx->P + g] = (int64_t)len[ctx->P + ctx->inv[g]];
+    return GLS_OK;
+}
+
+int gls_get_waveforms(gls_ctx* ctx, int64_t* offsets, uint64_t* tr, int64_t capacity, int64_t* total_out) {
+    if (!ctx) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    const int64_t N = (int64_t)ctx->P + ctx->G;
+    std::vector<unsigned long long> len((size_t)N);
+    std::vector<uint32_t> nck((size_t)N), nck_n((size_t)N);
+    if (N) {
+        CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(nck.data(), ctx->d_net_ck.p, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(nck_n.data(), ctx->d_net_nck.p, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost));
+    }
+    auto internal = [&](int64_t u) -> int64_t { return u < ctx->P ? u : ctx->P + ctx->inv[u - ctx->P]; };
+    int64_t total = 0;
+    for (int64_t u = 0; u < N; ++u) {
+        if (offsets) offsets[u] = total;
+        total += (int64_t)len[(size_t)internal(u)];
+    }
+    if (offsets) offsets[N] = total;
+    if (total_out) *total_out = total;
+    if (!tr) return GLS_OK;
+    if (capacity < total) return fail(ctx, GLS_ERANGE, "capacity %lld < %lld transitions", (long long)capacity, (long long)total);
+    const size_t nchunks = (size_t)ctx->last.chunk_top;
+    std::vector<unsigned long long> ck_off(nchunks);
+    std::vector<uint32_t> ck_cnt(nchunks);
+    if (nchunks) {
+        CK(cudaMemcpy(ck_off.data(), ctx->d_ck_off.p, sizeof(unsigned long long) * nchunks, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ck_cnt.data(), ctx->d_ck_cnt.p, sizeof(uint32_t) * nchunks, cudaMemcpyDeviceToHost));
+    }
+    std::vector<uint64_t> arena((size_t)ctx->last.arena_top);
+    if (!arena.empty())
+        CK(cudaMemcpy(arena.data(), ctx->d_arena.p, sizeof(uint64_t) * arena.size(), cudaMemcpyDeviceToHost));
+    int64_t o = 0;
+    for (int64_t u = 0; u < N; ++u) {
+        int64_t n = internal(u);
+        for (uint32_t j = nck[n]; j < nck[n] + nck_n[n]; ++j) {
+            std::memcpy(tr + o, arena.data() + ck_off[j], sizeof(uint64_t) * ck_cnt[j]);
+            o += ck_cnt[j];
+        }
+    }
+    return GLS_OK;
+}
+
+int gls_get_net_hashes_device(gls_ctx* ctx, uint64_t* d_hashes) {
+    if (!ctx || !d_hashes) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    cudaSetDevice(ctx->device);
+    CK(launch_hashes(params(ctx), ctx->d_perm.p, d_hashes, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GLS_OK;
+}
+
+int gls_get_net_hashes(gls_ctx* ctx, uint64_t* hashes) {
+    if (!ctx || !hashes) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    const int64_t N = (int64_t)ctx->P + ctx->G;
+    DevBuf<uint64_t> d;
+    CK(d.alloc(N));
+    int rc = gls_get_net_hashes_device(ctx, d.p);
+    if (rc) return rc;
+    if (N) CK(cudaMemcpy(hashes, d.p, sizeof(uint64_t) * N, cudaMemcpyDeviceToHost));
+    return GLS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,97 @@
+// gls_internal.cuh — device data layout shared by the host API (gls_api.cu) and
+// the kernels (gls_kernels.cu).  Product code: shares nothing with oracle/.
+//
+// Layout:
+//   nets      0..P-1 given (PI / pseudo-PI), P+i output of internal gate i;
+//             internal gates are sorted by topological level.
+//   arena     one u64 store for given and computed waveforms (the paper keeps
+//             both in one CSRP store); entries (t << 2) | v.
+//   chunks    a net's waveform is a time-ordered list of chunk segments; chunk
+//             j holds the net's transitions with t in [ck_T[j], ck_T[j+1]) at
+//             arena[ck_off[j] .. + ck_cnt[j]).  Given nets have one chunk.
+//             A gate's chunks are its (gate, time-chunk) work items.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gls {
+
+constexpr int kNumTypes = 9;
+constexpr int kLutPerType = 4 + 16 + 64 + 256;       // arity 1..4, index = packed 2-bit codes
+constexpr int kLutBytes = kLutPerType * kNumTypes;   // 3060 B, staged in shared memory
+constexpr uint64_t kInfEntry = ~0ull;                // head of an exhausted cursor
+constexpr int kRing = 32;                            // on-chip pending-schedule ring (power of 2)
+constexpr int kThreads = 256;                        // persistent-kernel CTA size
+
+__host__ __device__ inline int lut_offset(int type, int arity) {
+    // offset of (type, arity) table; arity 1 -> 0, 2 -> 4, 3 -> 20, 4 -> 84
+    return type * kLutPerType + (arity == 1 ? 0 : arity == 2 ? 4 : arity == 3 ? 20 : 84);
+}
+
+struct GateInfo {
+    uint32_t pin_off;   // first pin in pin_src / pin_delay
+    uint16_t lut_base;  // lut_offset(type, arity)
+    uint8_t k;          // arity 1..4
+    uint8_t pad;
+};
+
+enum : unsigned { kErrArena = 1u, kErrChunks = 2u, kErrDeep = 4u, kErrInput = 8u, kErrBug = 16u };
+
+// device control block, initialised by the host before each run
+struct Ctl {
+    unsigned long long chunk_top;   // next free chunk id (starts at P: one chunk per given net)
+    unsigned long long arena_top;   // next free arena entry (starts after the given waveforms)
+    unsigned long long deep_top;    // deep-backtrace scratch bump pointer (reset per level)
+    unsigned int bar_count;
+    unsigned int bar_gen;
+    unsigned int bar_abort;
+    unsigned int error;             // kErr* bits
+    unsigned long long need_arena;  // entries needed when kErrArena was raised
+    unsigned long long need_chunks;
+    unsigned long long need_deep;
+    unsigned long long gate_evals;
+    unsigned long long events;
+    unsigned long long out_trans;
+    unsigned long long chunks;
+    unsigned long long deep_chunks;
+};
+
+struct SimParams {
+    int32_t P, G, L;
+    const int32_t* level_off;   // [L+1] internal gate index ranges per level
+    const GateInfo* gate;       // [G]
+    const uint32_t* pin_src;    // [E] internal net id of each pin's driver
+    const uint4* pin_delay;     // [E] (rise->0, rise->1, fall->0, fall->1)
+    const uint8_t* lut;         // [kLutBytes]
+    uint64_t* arena;
+    unsigned long long arena_cap;     // entries
+    uint32_t* net_ck;           // [P+G] first chunk id
+    uint32_t* net_nck;          // [P+G] number of chunks
+    unsigned long long* net_len;      // [P+G] transitions
+    long long* ck_T;            // [ck_cap] chunk start time
+    unsigned long long* ck_off; // [ck_cap] arena offset of the chunk segment
+    uint32_t* ck_cnt;           // [ck_cap] entries in the segment
+    unsigned long long* ck_cum; // [ck_cap] entries of the net before this chunk
+    uint8_t* ck_vb;             // [ck_cap] net value just before ck_T (for halo starts)
+    uint32_t* ck_gate;          // [ck_cap] internal gate of the chunk
+    unsigned long long ck_cap;
+    uint32_t* gate_done;        // [G] finished chunks per gate
+    unsigned long long* work;   // [L+1] per-level work counters
+    uint64_t* deep;             // deep-backtrace scratch
+    unsigned long long deep_cap;
+    Ctl* ctl;
+    long long duration;
+    int32_t M;                  // target merged input events per chunk
+    int32_t ring_cap;           // <= kRing
+    uint32_t nblocks;
+};
+
+// kernels / launchers (gls_kernels.cu)
+cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaStream_t s);
+cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s);
+int max_coresident_blocks(int device, int* per_sm);
+cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
+                                   unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s);
+cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s);
+
+}  // namespace gls

@@ -1,0 +1,587 @@
+// gls_kernels.cu — sm_100a kernels of the gate-level re-simulation hot path.
+//
+// One persistent cooperative kernel (sim_kernel) runs the whole netlist in one
+// pass with no host round trip (the paper's one-pass property):
+// for each topological level it (A) plans (gate, time-chunk) work items and
+// (B) evaluates them, separated by device-wide barriers.  Each work item runs
+// Algorithm 2 over its chunk of time with an exact halo, applies
+// the Eq. 1 glitch filter with a streaming-finality rule, counts,
+// allocates its exact output segment (warp-aggregated bump allocation, the
+// atomic page iterator of P:499 without page waste) and writes it.
+// DESIGN.md §4-§5 give the derivations; the kernel is checked bit-exactly
+// against oracle/ by tests/test_gpu_parity.py.
+#include "gls_internal.cuh"
+
+namespace gls {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Device-wide barrier for a co-resident (cooperative) grid.  The last block to
+// arrive publishes the abort decision (any error raised before the barrier),
+// so every block takes the same branch afterwards.
+__device__ bool grid_barrier(Ctl* ctl, unsigned nblocks, unsigned& gen) {
+    __shared__ unsigned s_abort;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+        if (arrived == nblocks - 1) {
+            ctl->bar_count = 0;
+            ctl->bar_abort = (*(volatile unsigned*)&ctl->error) != 0u;
+            __threadfence();
+            st_release_u32(&ctl->bar_gen, gen + 1);
+        } else {
+            while (ld_acquire_u32(&ctl->bar_gen) == gen) __nanosleep(40);
+        }
+        __threadfence();  // gpu-scope fence also invalidates this SM's L1
+        s_abort = *(volatile unsigned*)&ctl->bar_abort;
+        gen = gen + 1;
+    }
+    __syncthreads();
+    return s_abort != 0u;
+}
+
+__device__ __forceinline__ unsigned warp_incl_scan(unsigned x) {
+    const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (unsigned)o) x += y;
+    }
+    return x;
+}
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+// Z is read as X: code 3 -> 2.
+__device__ __forceinline__ uint32_t norm_code(uint32_t v) { return v ^ ((v >> 1) & v & 1u); }
+// rank in the order 0 < X < 1 (reading R2): 0->0, 2(X)->1, 1->2
+__device__ __forceinline__ uint32_t rank_code(uint32_t f) { return ((f & 1u) << 1) | (f >> 1); }
+
+__device__ __forceinline__ long long etime(uint64_t e) { return (long long)(e >> 2); }
+
+// time of the idx-th transition of a net (idx < net_len)
+__device__ long long time_at(const SimParams& p, uint32_t net, unsigned long long idx) {
+    uint32_t cb = p.net_ck[net], n = p.net_nck[net];
+    uint32_t lo = 0, hi = n;  // largest j with cum[cb+j] <= idx
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (p.ck_cum[cb + mid] <= idx) lo = mid; else hi = mid;
+    }
+    uint32_t j = cb + lo;
+    return etime(p.arena[p.ck_off[j] + (idx - p.ck_cum[j])]);
+}
+
+// Cursor over one fan-in net's transitions (across its chunk segments).
+struct Cursor {
+    const uint64_t* ptr;
+    const uint64_t* end;
+    uint32_t ck, ck_end;
+};
+
+__device__ __forceinline__ void refill(const SimParams& p, Cursor& c) {
+    while (c.ptr == c.end && c.ck + 1 < c.ck_end) {
+        ++c.ck;
+        unsigned long long off = p.ck_off[c.ck];
+        uint32_t cnt = p.ck_cnt[c.ck];
+        c.ptr = p.arena + off;
+        c.end = c.ptr + cnt;
+    }
+}
+__device__ __forceinline__ uint64_t head(const Cursor& c) { return c.ptr < c.end ? *c.ptr : kInfEntry; }
+
+// Position a cursor at the first transition with t > tau0; *init = the net's
+// value at tau0 (X if none).  Uses the chunk start times and each chunk's
+// value-before (ck_vb) so no backward walk is needed.
+__device__ void locate(const SimParams& p, uint32_t net, long long tau0, Cursor& c, uint32_t& init) {
+    uint32_t cb = p.net_ck[net], n = p.net_nck[net];
+    uint32_t lo = 0, hi = n;  // largest j with ck_T[j] <= tau0 + 1 (default 0)
+    while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (p.ck_T[cb + mid] <= tau0 + 1) lo = mid; else hi = mid;
+    }
+    uint32_t j = cb + lo;
+    const uint64_t* seg = p.arena + p.ck_off[j];
+    uint32_t cnt = p.ck_cnt[j];
+    uint32_t a = 0, b = cnt;  // first index with t > tau0
+    while (a < b) {
+        uint32_t m = (a + b) >> 1;
+        if (etime(seg[m]) <= tau0) a = m + 1; else b = m;
+    }
+    init = a > 0 ? (uint32_t)(seg[a - 1] & 3u) : (uint32_t)p.ck_vb[j];
+    c.ptr = seg + a;
+    c.end = seg + cnt;
+    c.ck = j;
+    c.ck_end = cb + n;
+    refill(p, c);
+}
+
+struct ChunkSetup {
+    uint32_t src[4];
+    uint4 d[4];
+    uint32_t k, lut_base, dmin;
+    long long T0, T1, tau0;
+};
+
+struct ChunkOut {
+    uint32_t cnt;       // output transitions in [T0, min(T1-1, duration)]
+    uint32_t evals;     // distinct input timestamps in [T0, T1)
+    uint32_t events;    // zero-delay output changes at timestamps in [T0, T1)
+    uint32_t vb;        // output value just before T0
+    bool overflow;      // pending ring overflow (local ring only)
+};
+
+// Count input transitions of the chunk window (tau0, T1): bound for the deep ring.
+__device__ unsigned long long window_bound(const SimParams& p, const ChunkSetup& s) {
+    unsigned long long n = 2;
+    for (uint32_t i = 0; i < s.k; ++i) {
+        Cursor c;
+        uint32_t init;
+        locate(p, s.src[i], s.tau0, c, init);
+        for (;;) {
+            uint64_t h = head(c);
+            if (h == kInfEntry || etime(h) >= s.T1) break;
+            ++n;
+            ++c.ptr;
+            if (c.ptr == c.end) refill(p, c);
+        }
+    }
+    return n;
+}
+
+// One pass of Algorithm 2 over a chunk.  DEEP selects the pending-schedule
+// storage: a 32-entry ring in local memory, or a linear array in global
+// scratch sized by window_bound (exact for any backtrace depth, reading R13).
+template <bool WRITE, bool DEEP>
+__device__ void run_chunk(const SimParams& p, const ChunkSetup& s, const uint8_t* lut,
+                          uint64_t* out, uint64_t* dbuf, unsigned long long dcap, ChunkOut& r) {
+    uint64_t lring[DEEP ? 1 : kRing];
+    uint64_t* ring = DEEP ? dbuf : lring;
+    const unsigned long long cap = DEEP ? dcap : (unsigned long long)p.ring_cap;
+    const unsigned long long mask = DEEP ? ~0ull : (unsigned long long)(kRing - 1);
+
+    Cursor cur[4];
+    uint64_t h[4];
+    uint32_t xn = 0, x0 = 0;  // packed normalised input codes, 2 bits per pin
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        h[i] = kInfEntry;
+        if ((uint32_t)i < s.k) {
+            uint32_t init;
+            locate(p, s.src[i], s.tau0, cur[i], init);
+            h[i] = head(cur[i]);
+            xn |= 2u << (2 * i);                      // all inputs start at X
+            x0 |= norm_code(init) << (2 * i);         // values in effect at tau0
+        }
+    }
+    uint32_t Eprev = 2;          // previous zero-delay evaluation, X
+    unsigned long long lo = 0, hi = 0;
+    uint32_t lastv = 2;          // value of the last finalised schedule (X before any)
+    uint32_t vb = 2, cnt = 0, evals = 0, events = 0;
+    bool overflow = false;
+    const long long T0 = s.T0, T1 = s.T1, dur = p.duration;
+    const long long dmin = (long long)s.dmin;
+
+    auto emit = [&](uint64_t e) {
+        long long rr = etime(e);
+        if (rr < T0) {
+            vb = (uint32_t)(e & 3u);
+        } else if (rr < T1 && rr <= dur) {
+            if (WRITE) out[cnt] = e;
+            ++cnt;
+        }
+        lastv = (uint32_t)(e & 3u);
+    };
+
+    // one distinct timestamp t with post-update input vector nx (Alg. 2 body)
+    auto step = [&](long long t, uint32_t nx) {
+        if (nx != xn) {
+            uint32_t E = lut[s.lut_base + nx];                   // calculateSignals
+            if (E != Eprev) {                                    // "o_k.v is changed" (R4a)
+                uint32_t del = 0xffffffffu;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    uint32_t fo = (xn >> (2 * i)) & 3u, fn = (nx >> (2 * i)) & 3u;
+                    if (fo != fn) {                              // changed inputs only (R3)
+                        bool rise = rank_code(fn) > rank_code(fo);
+                        uint32_t a = rise ? s.d[i].x : s.d[i].z;  // -> 0
+                        uint32_t b = rise ? s.d[i].y : s.d[i].w;  // -> 1
+                        uint32_t dd = E == 0u ? a : (E == 1u ? b : min(a, b));   // R1
+                        del = min(del, dd);                      // min rule
+                    }
+                }
+                long long rr = t + (long long)del;               // o_k.t = t + del
+                // addSignalChange with Eq. 1: deny pending schedules at >= rr
+                while (hi != lo && etime(ring[(hi - 1) & mask]) >= rr) --hi;
+                uint32_t tv = hi != lo ? (uint32_t)(ring[(hi - 1) & mask] & 3u) : lastv;
+                if (tv != E) {
+                    if (hi - lo >= cap) {
+                        overflow = true;
+                    } else {
+                        ring[hi & mask] = ((uint64_t)rr << 2) | E;
+                        ++hi;
+                    }
+                }
+                if (t >= T0) ++events;
+                Eprev = E;
+            }
+            xn = nx;
+        }
+        // streaming finality: later schedules appear after t + dmin, so they
+        // can only deny entries beyond it
+        const long long lim = t + dmin;
+        while (hi != lo && etime(ring[lo & mask]) <= lim) {
+            emit(ring[lo & mask]);
+            ++lo;
+        }
+    };
+
+    step(s.tau0, x0);  // the halo start: inputs take their values at tau0
+    for (;;) {
+        if (overflow) break;
+        uint64_t m = min(min(h[0], h[1]), min(h[2], h[3]));
+        long long t = etime(m);
+        if (m == kInfEntry || t >= T1) break;
+        uint32_t nx = xn;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (etime(h[i]) == t && h[i] != kInfEntry) {
+                nx = (nx & ~(3u << (2 * i))) | (norm_code((uint32_t)(h[i] & 3u)) << (2 * i));
+                ++cur[i].ptr;
+                if (cur[i].ptr == cur[i].end) refill(p, cur[i]);
+                h[i] = head(cur[i]);
+            }
+        }
+        if (t >= T0) ++evals;
+        step(t, nx);
+    }
+    // everything pending that appears before T1 is final for this chunk
+    while (hi != lo && etime(ring[lo & mask]) < T1) {
+        emit(ring[lo & mask]);
+        ++lo;
+    }
+    r.cnt = cnt;
+    r.evals = evals;
+    r.events = events;
+    r.vb = vb;
+    r.overflow = overflow;
+}
+
+// ------------------------------------------------------------------ phase A
+// Plan level l: every gate gets ceil(n_in / M) chunks (n_in = Σ fan-in lengths,
+// at most len(ref)+1 where ref = longest fan-in); chunk ids are bump-allocated
+// per warp and each chunk records its gate.
+__device__ void plan_level(const SimParams& p, int l, unsigned gwarp, unsigned nwarps) {
+    const unsigned lane = threadIdx.x & 31;
+    const int g0 = p.level_off[l - 1], g1 = p.level_off[l];
+    const int n = g1 - g0;
+    for (int base = (int)gwarp * 32; base < n; base += (int)nwarps * 32) {
+        const int gi = g0 + base + (int)lane;
+        const bool v = base + (int)lane < n;
+        unsigned nch = 0;
+        if (v) {
+            GateInfo g = p.gate[gi];
+            unsigned long long n_in = 0, lenref = 0;
+            for (uint32_t i = 0; i < g.k; ++i) {
+                unsigned long long len = p.net_len[p.pin_src[g.pin_off + i]];
+                n_in += len;
+                if (len > lenref) lenref = len;
+            }
+            unsigned long long c = (n_in + (unsigned long long)p.M - 1) / (unsigned long long)p.M;
+            if (c < 1) c = 1;
+            if (c > lenref + 1) c = lenref + 1;
+            nch = (unsigned)c;
+        }
+        unsigned incl = warp_incl_scan(nch);
+        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long wb = 0;
+        if (lane == 31) wb = atomicAdd(&p.ctl->chunk_top, (unsigned long long)total);
+        wb = __shfl_sync(0xffffffffu, wb, 31);
+        if (wb + total > p.ck_cap) {
+            if (lane == 0) {
+                atomicOr(&p.ctl->error, kErrChunks);
+                atomicMax(&p.ctl->need_chunks, wb + total);
+            }
+            continue;
+        }
+        unsigned long long my = wb + incl - nch;
+        if (v) {
+            p.net_ck[p.P + gi] = (uint32_t)my;
+            p.net_nck[p.P + gi] = nch;
+            p.gate_done[gi] = 0;
+        }
+        // the warp writes the chunk -> gate map of its 32 gates cooperatively
+        for (int j = 0; j < 32; ++j) {
+            unsigned nj = __shfl_sync(0xffffffffu, nch, j);
+            unsigned long long bj = __shfl_sync(0xffffffffu, my, j);
+            for (unsigned c = lane; c < nj; c += 32) p.ck_gate[bj + c] = (uint32_t)(g0 + base + j);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ phase B
+__device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetup& s,
+                            uint32_t& g_out, uint32_t& c_out, uint32_t& nch_out) {
+    const uint32_t gi = p.ck_gate[id];
+    const GateInfo g = p.gate[gi];
+    const uint32_t base = p.net_ck[p.P + gi], nch = p.net_nck[p.P + gi];
+    const uint32_t c = (uint32_t)(id - base);
+    s.k = g.k;
+    s.lut_base = g.lut_base;
+    unsigned long long lenref = 0;
+    uint32_t ref = 0;
+    uint32_t dmin = 0xffffffffu, dmax = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if ((uint32_t)i < g.k) {
+            uint32_t src = p.pin_src[g.pin_off + i];
+            s.src[i] = src;
+            uint4 d = p.pin_delay[g.pin_off + i];
+            s.d[i] = d;
+            dmin = min(dmin, min(min(d.x, d.y), min(d.z, d.w)));
+            dmax = max(dmax, max(max(d.x, d.y), max(d.z, d.w)));
+            unsigned long long len = p.net_len[src];
+            if (len > lenref) { lenref = len; ref = src; }
+        } else {
+            s.src[i] = 0;
+            s.d[i] = make_uint4(0, 0, 0, 0);
+        }
+    }
+    s.dmin = dmin;
+    // chunk boundaries: quantiles of the longest fan-in's transition times
+    auto bound = [&](uint32_t cc) -> long long {
+        unsigned long long q = lenref / nch, rm = lenref % nch;
+        unsigned long long idx = (unsigned long long)cc * q + ((unsigned long long)cc * rm) / nch;
+        return time_at(p, ref, idx);
+    };
+    s.T0 = c == 0 ? 0 : bound(c);
+    s.T1 = c + 1 == nch ? p.duration + 1 : bound(c + 1);
+    // halo: H = dmax + 1 (reading R17 for one gate); tau0 may be negative
+    s.tau0 = s.T0 - (long long)dmax - 1;
+    g_out = gi;
+    c_out = c;
+    nch_out = nch;
+}
+
+__device__ void process_level(const SimParams& p, unsigned long long ck_begin, unsigned long long ck_end,
+                              unsigned long long* work, const uint8_t* lut) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long n = ck_end - ck_begin;
+    for (;;) {
+        unsigned long long wb = 0;
+        if (lane == 0) wb = atomicAdd(work, 32ull);
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if (wb >= n) break;
+        const unsigned long long id = ck_begin + wb + lane;
+        const bool active = wb + lane < n;
+
+        ChunkSetup s;
+        ChunkOut r{0, 0, 0, 2, false};
+        uint32_t gi = 0, c = 0, nch = 1;
+        bool deep = false;
+        uint64_t* dbuf = nullptr;
+        unsigned long long dcap = 0;
+        if (active) {
+            setup_chunk(p, id, s, gi, c, nch);
+            run_chunk<false, false>(p, s, lut, nullptr, nullptr, 0, r);
+            if (r.overflow) {
+                // deep backtrace: exact path with a scratch ring sized by the window
+                deep = true;
+                dcap = window_bound(p, s);
+                unsigned long long at = atomicAdd(&p.ctl->deep_top, dcap);
+                atomicAdd(&p.ctl->deep_chunks, 1ull);
+                if (at + dcap > p.deep_cap) {
+                    atomicOr(&p.ctl->error, kErrDeep);
+                    atomicMax(&p.ctl->need_deep, at + dcap);
+                    deep = false;
+                    r.cnt = 0;
+                } else {
+                    dbuf = p.deep + at;
+                    run_chunk<false, true>(p, s, lut, nullptr, dbuf, dcap, r);
+                    if (r.overflow) atomicOr(&p.ctl->error, kErrBug);
+                }
+            }
+        }
+        // exact output allocation: warp scan + one bump per warp (no page waste)
+        unsigned incl = warp_incl_scan(r.cnt);
+        unsigned total = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long ab = 0;
+        if (lane == 31) ab = atomicAdd(&p.ctl->arena_top, (unsigned long long)total);
+        ab = __shfl_sync(0xffffffffu, ab, 31);
+        const bool fits = ab + total <= p.arena_cap;
+        if (!fits && lane == 0) {
+            atomicOr(&p.ctl->error, kErrArena);
+            atomicMax(&p.ctl->need_arena, ab + total);
+        }
+        const unsigned long long my = ab + incl - r.cnt;
+        if (active && fits) {
+            ChunkOut r2{0, 0, 0, 2, false};
+            if (deep)
+                run_chunk<true, true>(p, s, lut, p.arena + my, dbuf, dcap, r2);
+            else
+                run_chunk<true, false>(p, s, lut, p.arena + my, nullptr, 0, r2);
+            if (r2.cnt != r.cnt) atomicOr(&p.ctl->error, kErrBug);
+            p.ck_T[id] = s.T0;
+            p.ck_off[id] = my;
+            p.ck_cnt[id] = r.cnt;
+            p.ck_vb[id] = (uint8_t)r.vb;
+            __threadfence();
+            unsigned prev = atomicAdd(&p.gate_done[gi], 1u);
+            if (prev == nch - 1) {
+                // last chunk of the gate: prefix counts + net length
+                __threadfence();
+                const uint32_t base = p.net_ck[p.P + gi];
+                unsigned long long cum = 0;
+                for (uint32_t j = 0; j < nch; ++j) {
+                    p.ck_cum[base + j] = cum;
+                    cum += __ldcg(&p.ck_cnt[base + j]);
+                }
+                p.net_len[p.P + gi] = cum;
+            }
+        }
+        unsigned long long se = warp_sum64(active ? r.evals : 0u);
+        unsigned long long sv = warp_sum64(active ? r.events : 0u);
+        unsigned long long sc = warp_sum64(active ? 1ull : 0ull);
+        if (lane == 0) {
+            atomicAdd(&p.ctl->gate_evals, se);
+            atomicAdd(&p.ctl->events, sv);
+            atomicAdd(&p.ctl->out_trans, (unsigned long long)total);
+            atomicAdd(&p.ctl->chunks, sc);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) sim_kernel(SimParams p) {
+    __shared__ uint8_t s_lut[kLutBytes];
+    for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) s_lut[i] = p.lut[i];
+    __syncthreads();
+    const unsigned warps_per_block = blockDim.x >> 5;
+    const unsigned gwarp = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
+    const unsigned nwarps = gridDim.x * warps_per_block;
+    unsigned gen = 0;
+    unsigned long long ck_begin = (unsigned long long)p.P;
+    for (int l = 1; l <= p.L; ++l) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) p.ctl->deep_top = 0;
+        plan_level(p, l, gwarp, nwarps);
+        if (grid_barrier(p.ctl, p.nblocks, gen)) return;
+        const unsigned long long ck_end = *(volatile unsigned long long*)&p.ctl->chunk_top;
+        process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
+        if (grid_barrier(p.ctl, p.nblocks, gen)) return;
+        ck_begin = ck_end;
+    }
+}
+
+// given nets: one chunk each, covering the whole duration
+__global__ void init_given_kernel(SimParams p, const long long* in_off) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.P; i += gridDim.x * blockDim.x) {
+        long long a = in_off[i], b = in_off[i + 1];
+        p.net_ck[i] = (uint32_t)i;
+        p.net_nck[i] = 1;
+        p.net_len[i] = (unsigned long long)(b - a);
+        p.ck_T[i] = 0;
+        p.ck_off[i] = (unsigned long long)a;
+        p.ck_cnt[i] = (uint32_t)(b - a);
+        p.ck_cum[i] = 0;
+        p.ck_vb[i] = 2;
+        p.ck_gate[i] = 0xffffffffu;
+    }
+}
+
+// validation of device-resident given waveforms (same rules as the host path)
+__global__ void validate_kernel(int32_t P, const long long* off, const uint64_t* tr, long long total,
+                                unsigned* err, unsigned long long* maxt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        long long a = off[i], b = off[i + 1];
+        if (a < 0 || b < a || b > total) { atomicOr(err, 1u); continue; }
+        uint32_t prev = 2;
+        long long pt = -1;
+        for (long long j = a; j < b; ++j) {
+            uint64_t e = tr[j];
+            long long t = (long long)(e >> 2);
+            uint32_t v = (uint32_t)(e & 3u);
+            if (t <= pt || v == prev || t >= (1ll << 61)) { atomicOr(err, 2u); break; }
+            prev = v;
+            pt = t;
+        }
+        if (pt >= 0) atomicMax(maxt, (unsigned long long)pt);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && off[0] != 0) atomicOr(err, 1u);
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// per-net hash, written in user net order
+__global__ void hash_kernel(SimParams p, const uint32_t* perm, uint64_t* out) {
+    const int N = p.P + p.G;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+        uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
+        uint64_t h = splitmix64(0x9E3779B97F4A7C15ull ^ (uint64_t)p.net_len[n]);
+        for (uint32_t j = cb; j < cb + nck; ++j) {
+            const uint64_t* s = p.arena + p.ck_off[j];
+            uint32_t c = p.ck_cnt[j];
+            for (uint32_t q = 0; q < c; ++q) h = splitmix64(h ^ s[q]);
+        }
+        int user = n < p.P ? n : p.P + (int)perm[n - p.P];
+        out[user] = h;
+    }
+}
+
+// ------------------------------------------------------------------ launchers
+int max_coresident_blocks(int device, int* per_sm) {
+    int nb = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel, kThreads, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    if (per_sm) *per_sm = nb;
+    return nb * sms;
+}
+
+cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s) {
+    SimParams q = p;
+    q.nblocks = (uint32_t)blocks;
+    void* args[] = {&q};
+    return cudaLaunchCooperativeKernel((void*)sim_kernel, dim3(blocks), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaStream_t s) {
+    if (p.P == 0) return cudaSuccess;
+    int blocks = (p.P + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    init_given_kernel<<<blocks, 256, 0, s>>>(p, in_off);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
+                                   unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s) {
+    int blocks = (P + 255) / 256;
+    if (blocks < 1) blocks = 1;
+    if (blocks > 4096) blocks = 4096;
+    validate_kernel<<<blocks, 256, 0, s>>>(P, off, tr, total, d_err, d_maxt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s) {
+    int N = p.P + p.G;
+    if (N == 0) return cudaSuccess;
+    int blocks = (N + 255) / 256;
+    if (blocks > 8192) blocks = 8192;
+    hash_kernel<<<blocks, 256, 0, s>>>(p, perm, out);
+    return cudaGetLastError();
+}
+
+}  // namespace gls

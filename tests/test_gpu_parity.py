@@ -1,0 +1,223 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle,
+bit-exact on every transition time and value of every net, plus the oracle's
+counts (gate-evals, events, output transitions) and per-net hashes."""
+import numpy as np
+import pytest
+import torch
+
+import golden_io
+from oracle import oracle
+from paper_2304_13398_b200 import gls
+from paper_2304_13398_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = gls.Context(0)
+    yield c
+    c.close()
+
+
+def run_oracle(nl, st, dur):
+    return oracle.simulate(nl.num_inputs, nl.gate_type, nl.fanin_offsets, nl.fanin_net,
+                           nl.pin_delay, st.offsets, st.trans, dur)
+
+
+def run_gpu(c, nl, st, dur, **cfg):
+    c.gls_set_config(**cfg)
+    c.load(nl)
+    c.gls_set_input_waveforms(nl.num_inputs, st.offsets, st.trans)
+    c.gls_simulate(dur)
+    return c.gls_get_waveforms(), c.gls_get_stats()
+
+
+def assert_same(c, nl, st, dur, ref=None, hashes=True, **cfg):
+    ref = ref or run_oracle(nl, st, dur)
+    w, s = run_gpu(c, nl, st, dur, **cfg)
+    if not np.array_equal(w.offsets, ref.offsets) or not np.array_equal(w.trans, ref.trans):
+        for n in range(nl.num_nets):
+            if w.wave(n) != ref.wave(n):
+                raise AssertionError(f"net {n} differs: gpu {w.wave(n)[:20]} oracle {ref.wave(n)[:20]}")
+        raise AssertionError("csr differs")
+    assert s["gate_evals"] == ref.gate_evals
+    assert s["events"] == ref.events
+    assert s["out_transitions"] == ref.out_trans
+    if hashes:
+        assert np.array_equal(c.gls_get_net_hashes(), ref.hashes)
+    return s
+
+
+@pytest.mark.parametrize("ex", golden_io.examples(), ids=lambda e: e.name)
+def test_worked_examples(ctx, ex):
+    nl, st, dur, index, exp = ex.build()
+    w, _ = run_gpu(ctx, nl, st, dur)
+    for net, wave in exp.items():
+        assert w.wave(net) == wave, (ex.name, nl.names[net])
+    assert_same(ctx, nl, st, dur)
+
+
+def test_random_designs_1000(ctx):
+    """SPEC-style acceptance: >= 1000 random designs."""
+    rng = np.random.Generator(np.random.PCG64(2024))
+    for d in range(1000):
+        P = int(rng.integers(1, 12))
+        G = int(rng.integers(1, 120))
+        nl = W.random_dag(10_000 + d, P, G, max_delay=int(rng.integers(0, 15)))
+        st = W.random_stimuli(d, P, int(rng.integers(0, 40)), 400, xz=float(rng.random() * 0.3),
+                              max_gap=int(rng.integers(1, 30)))
+        try:
+            assert_same(ctx, nl, st, 450, hashes=(d % 10 == 0))
+        except AssertionError as e:
+            raise AssertionError(f"design {d}: {e}")
+
+
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 17])
+def test_small_chunks_exact(ctx, M):
+    """Many (gate, time-chunk) items per gate: halo starts, chunk value-before
+    and cross-chunk cursors all exercised."""
+    for seed in range(15):
+        nl = W.random_dag(500 + seed, 6, 80, max_delay=20)
+        st = W.random_stimuli(seed, 6, 60, 3000, xz=0.1, max_gap=60)
+        assert_same(ctx, nl, st, 3100, chunk_events=M, hashes=False)
+
+
+@pytest.mark.parametrize("ring", [1, 2, 3])
+def test_deep_backtrace_path(ctx, ring):
+    """Pending-schedule ring overflow -> exact deep path (reading R13)."""
+    deep = 0
+    for seed in range(12):
+        nl = W.random_dag(700 + seed, 5, 60, max_delay=40)
+        st = W.random_stimuli(seed, 5, 80, 800, xz=0.2, max_gap=4)
+        s = assert_same(ctx, nl, st, 900, ring_limit=ring, chunk_events=int(8 + seed), hashes=False)
+        deep += s["deep_chunks"]
+    assert deep > 0
+
+
+def test_zero_and_huge_delays(ctx):
+    for seed in range(10):
+        nl = W.random_dag(800 + seed, 4, 50, max_delay=0)
+        st = W.random_stimuli(seed, 4, 30, 200, xz=0.3)
+        assert_same(ctx, nl, st, 250, hashes=False)
+    nl = W.random_dag(900, 4, 40, max_delay=10)
+    nl.pin_delay[::3] = (1 << 31) - 1
+    st = W.random_stimuli(9, 4, 30, 200)
+    assert_same(ctx, nl, st, 250)
+    assert_same(ctx, nl, st, (1 << 33))
+
+
+def test_large_times(ctx):
+    base = 1 << 59
+    nl = W.random_dag(901, 3, 30, max_delay=50)
+    waves = [[(base + 10 * j + p, (j + p) % 2) for j in range(20)] for p in range(3)]
+    st = W.stimuli_from_lists(waves)
+    assert_same(ctx, nl, st, (1 << 61) - 1)
+
+
+def test_empty_and_constant_inputs(ctx):
+    nl = W.random_dag(902, 4, 30, max_delay=5)
+    st = W.stimuli_from_lists([[], [], [], []])
+    assert_same(ctx, nl, st, 100)
+    st = W.stimuli_from_lists([[(0, 1)], [], [(5, 3)], [(0, 0), (7, 2)]])
+    assert_same(ctx, nl, st, 100)
+    # PIs only
+    nl0 = W.netlist_from_gates(2, [])
+    st0 = W.stimuli_from_lists([[(1, 0)], [(2, 3), (4, 1)]])
+    w, s = run_gpu(ctx, nl0, st0, 10)
+    assert w.wave(1) == [(2, 3), (4, 1)] and s["gate_evals"] == 0
+
+
+def test_c7552_shaped(ctx):
+    nl = W.config_netlist("c7552")
+    spec = W.config_stimspec("c7552")
+    o, t = W.generate_stimuli(spec)
+    st = W.Stimuli(o.numpy(), t.numpy().astype(np.uint64))
+    s = assert_same(ctx, nl, st, spec.duration)
+    assert s["gate_evals"] > 1_000_000
+
+
+def test_determinism_and_launch_shapes(ctx):
+    nl = W.recipe_netlist(5, 3000, 30, 200, shuffle=True)
+    spec = W.make_stimspec(5, 200, 300, "skewed", mean_trans=40, wcv=5.0)
+    o, t = W.generate_stimuli(spec)
+    st = W.Stimuli(o.numpy(), t.numpy().astype(np.uint64))
+    ref = run_oracle(nl, st, spec.duration)
+    base = None
+    for cfg in [dict(), dict(blocks_per_sm=1), dict(chunk_events=32), dict(chunk_events=4096), dict()]:
+        w, _ = run_gpu(ctx, nl, st, spec.duration, **cfg)
+        assert np.array_equal(w.trans, ref.trans)
+        if base is None:
+            base = w.trans.copy()
+        assert np.array_equal(base, w.trans)
+
+
+def test_device_inputs_and_resimulation(ctx):
+    nl = W.random_dag(903, 5, 100, max_delay=9)
+    ctx.gls_set_config()
+    ctx.load(nl)
+    for seed in range(3):
+        st = W.random_stimuli(seed, 5, 50, 1000)
+        ref = run_oracle(nl, st, 1100)
+        d_off = torch.as_tensor(st.offsets, device="cuda")
+        d_tr = torch.as_tensor(st.trans.astype(np.int64), device="cuda")
+        ctx.gls_set_input_waveforms_device(5, d_off.data_ptr(), d_tr.data_ptr(), st.total)
+        ctx.gls_simulate(1100)
+        w = ctx.gls_get_waveforms()
+        assert np.array_equal(w.trans, ref.trans)
+        d_h = torch.zeros(nl.num_nets, dtype=torch.int64, device="cuda")
+        ctx.gls_get_net_hashes_device(d_h.data_ptr())
+        assert np.array_equal(d_h.cpu().numpy().astype(np.uint64), ref.hashes)
+        cnt = ctx.gls_get_net_counts()
+        assert np.array_equal(cnt, np.diff(ref.offsets))
+
+
+def test_error_codes(ctx):
+    ok = W.random_dag(904, 2, 5)
+    with pytest.raises(gls.GlsError) as e:   # cycle
+        ctx.load(W.netlist_from_gates(1, [(W.AND, [0, 2], [(1,) * 4] * 2), (W.BUF, [1], [(1,) * 4])]))
+    assert e.value.code == gls.GLS_ECYCLE
+    for bad in [
+        W.netlist_from_gates(1, [(9, [0], [(1,) * 4])]),                        # unknown type
+        W.netlist_from_gates(1, [(W.AND, [0], [(1,) * 4])]),                    # arity
+        W.netlist_from_gates(1, [(W.BUF, [5], [(1,) * 4])]),                    # net id
+        W.netlist_from_gates(1, [(W.BUF, [0], [(1 << 31, 0, 0, 0)])]),          # delay
+    ]:
+        with pytest.raises(gls.GlsError) as e:
+            ctx.load(bad)
+        assert e.value.code == gls.GLS_EINVAL
+    ctx.load(ok)
+    with pytest.raises(gls.GlsError) as e:
+        ctx.gls_simulate(10)
+    assert e.value.code == gls.GLS_ESTATE
+    for waves in ([[(5, 1), (5, 0)], []], [[(1, 1), (2, 1)], []], [[(1, 2)], []]):
+        st = W.stimuli_from_lists(waves)
+        with pytest.raises(gls.GlsError) as e:
+            ctx.gls_set_input_waveforms(2, st.offsets, st.trans)
+        assert e.value.code == gls.GLS_EINVAL
+    st = W.stimuli_from_lists([[(50, 1)], []])
+    ctx.gls_set_input_waveforms(2, st.offsets, st.trans)
+    with pytest.raises(gls.GlsError) as e:
+        ctx.gls_simulate(40)
+    assert e.value.code == gls.GLS_ERANGE
+    ctx.gls_simulate(60)
+    assert ctx.gls_get_halo() >= 1
+
+
+def test_arena_too_small_reports_enomem():
+    nl = W.random_dag(905, 4, 200, max_delay=5)
+    st = W.random_stimuli(1, 4, 200, 5000)
+    with gls.Context(0) as c:
+        c.gls_set_config(arena_bytes=8 * (st.total + 16))
+        c.load(nl)
+        c.gls_set_input_waveforms(4, st.offsets, st.trans)
+        with pytest.raises(gls.GlsError) as e:
+            c.gls_simulate(6000)
+        assert e.value.code == gls.GLS_ENOMEM and "arena" in str(e.value)
+
+
+def test_generator_cpu_equals_gpu():
+    spec = W.make_stimspec(3, 300, 500, "skewed", mean_trans=30, wcv=4.0)
+    o1, t1 = W.generate_stimuli(spec, "cpu")
+    o2, t2 = W.generate_stimuli(spec, "cuda")
+    assert torch.equal(o1, o2.cpu()) and torch.equal(t1, t2.cpu())
