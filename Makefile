@@ -21,3 +21,7 @@ clean:
 	rm -f $(PKG)/libgls.so oracle/liboracle.so
 
 .PHONY: all clean ptxas
+
+# A/B variants for performance experiments (not used by tests)
+variant-%: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -DGLS_MINB=$* -shared -o /tmp/libgls_minb$*.so $(SRC) -lcudart

@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""bench.py — throughput of the gate-level re-simulation hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4_10m] [--impl gls|reference]
+
+A step is one gls_simulate: every gate of the netlist over the whole duration
+(all of SURVEY §8(a): plan, k-way merge, LUT, delays, Eq. 1 filter, exact
+allocation, levels), with the given waveforms already resident in HBM.  The
+value is gate-evaluations per second (metric of BASELINE.json), whole job.
+
+N = 1: the 10M-gate config (c4_10m) on one GPU.  N > 1 (torchrun): the same
+workload split into N time windows with a max-path-delay halo (strong scaling,
+DESIGN.md §4 / §8); rank 0 prints the JSON line with max-over-ranks timing.
+
+The default run also (rank 0 only) times the CPU oracle on a bounded prefix of
+the same workload (cpu_baseline) and checks the GPU's full-size run against it
+on that window (parity).  --impl reference times the oracle alone.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2304_13398_b200 import workloads as W  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+
+# prefix of the workload the oracle runs (cycles), sized for ~10-30 s of one core
+SAMPLE_CYCLES = {"c4_10m": 3000, "c3_1m": 60, "c7552": 1999, "c5_set": 150}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4_10m", choices=sorted(W.CONFIGS))
+    ap.add_argument("--impl", default="gls", choices=["gls", "reference"])
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sample-cycles", type=int, default=0)
+    ap.add_argument("--chunk-events", type=int, default=0)
+    ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--arena-gb", type=float, default=0.0)
+    return ap.parse_args()
+
+
+def log(*a):
+    print("[bench]", *a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy-based)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.dev)], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        time.sleep(0.25)
+        self.p.terminate()
+        try:
+            self.p.wait(5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) == 6:
+                    rows.append(parts)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def build_netlist(cfg, seed):
+    t = time.perf_counter()
+    nl = W.config_netlist(cfg, seed)
+    log(f"netlist {cfg}: {nl.num_gates} gates, {nl.num_inputs} PIs, {nl.num_pins} pins "
+        f"({time.perf_counter() - t:.1f}s)")
+    return nl
+
+
+def oracle_sample(nl, spec, cycles):
+    """The oracle as it stands on the workload's first `cycles` clock cycles."""
+    from oracle import oracle
+    o, t = W.window_stimuli(spec, 0, cycles, "cpu")
+    st = W.to_stimuli(o, t)
+    dur = cycles * W.PERIOD
+    t0 = time.perf_counter()
+    r = oracle.simulate(nl.num_inputs, nl.gate_type, nl.fanin_offsets, nl.fanin_net, nl.pin_delay,
+                        st.offsets, st.trans, dur, want_waves=False)
+    dt = time.perf_counter() - t0
+    return r, dt, dur
+
+
+def run_reference(a):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg = a.config
+    nl = build_netlist(cfg, a.seed)
+    spec = W.config_stimspec(cfg, a.seed)
+    cyc = max(1, (a.sample_cycles or SAMPLE_CYCLES[cfg]) // 4)
+    for _ in range(a.warmup):
+        oracle_sample(nl, spec, cyc)
+    evals, secs, outs = 0, 0.0, 0
+    for _ in range(a.steps):
+        r, dt, dur = oracle_sample(nl, spec, cyc)
+        evals += r.gate_evals
+        outs += r.out_trans
+        secs += dt
+    v = evals / secs
+    sample = (f"{cfg} netlist ({nl.num_gates} gates), first {cyc} of {spec.ncycles} clock cycles "
+              f"(t <= {cyc * W.PERIOD} ps), {r.gate_evals} gate-evals per step")
+    line = {"impl": "reference", "metric": "gate-evals/s", "value": v, "unit": "gate-evals/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * secs / a.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "int64", "data": "synthetic",
+            "config": {"workload": cfg, "gates": nl.num_gates, "pis": nl.num_inputs},
+            "output_transitions_per_s": outs / secs,
+            "cpu_baseline": {"value": v, "unit": "gate-evals/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "gate-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def window_hash_numpy(offsets, trans, t_lo, t_hi):
+    """Per-net hash of transitions with t_lo <= t <= t_hi, from a CSR."""
+    M = (1 << 64) - 1
+
+    def sm(x):
+        x = (x + 0x9E3779B97F4A7C15) & M
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+        return x ^ (x >> 31)
+    out = np.zeros(len(offsets) - 1, np.uint64)
+    for n in range(len(offsets) - 1):
+        e = trans[offsets[n]:offsets[n + 1]]
+        t = (e >> np.uint64(2)).astype(np.int64)
+        e = e[(t >= t_lo) & (t <= t_hi)]
+        h = sm(0x9E3779B97F4A7C15 ^ len(e))
+        for x in e:
+            h = sm(h ^ int(x))
+        out[n] = h
+    return out
+
+
+def run_gls(a):
+    from paper_2304_13398_b200 import gls
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = a.config
+    nl = build_netlist(cfg, a.seed)
+    spec = W.config_stimspec(cfg, a.seed)
+    stream = torch.cuda.current_stream(dev)
+    ctx = gls.Context(local, stream.cuda_stream)
+    ctx.gls_set_config(chunk_events=a.chunk_events, blocks_per_sm=a.blocks_per_sm,
+                       arena_bytes=int(a.arena_gb * (1 << 30)))
+    t = time.perf_counter()
+    ctx.load(nl)
+    L = ctx.gls_get_levels()
+    H = ctx.gls_get_halo()
+    log(f"loaded: {L} levels, halo {H} ps ({time.perf_counter() - t:.1f}s)")
+
+    # this rank's time window (strong scaling over the time axis; one window at N=1)
+    from paper_2304_13398_b200 import shard
+    nc = spec.ncycles
+    plan = shard.rank_plan(rank, world, nc, H, spec.duration)
+    k_hi = plan["gen_cycles"][1]
+    duration = plan["duration"]
+    t = time.perf_counter()
+    d_off, d_tr = W.window_stimuli(spec, *plan["gen_cycles"], dev)
+    torch.cuda.synchronize(dev)
+    n_in = int(d_tr.numel())
+    lens = (d_off[1:] - d_off[:-1]).double()
+    wcv = float(lens.std(unbiased=False) / lens.mean()) if n_in else 0.0
+    log(f"stimuli: {n_in} transitions on {spec.num_inputs} PIs, WCV {wcv:.2f} ({time.perf_counter() - t:.1f}s)")
+    ctx.gls_set_input_waveforms_device(nl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), n_in)
+
+    def step():
+        ctx.gls_simulate(duration)
+
+    for i in range(a.warmup):
+        t = time.perf_counter()
+        step()
+        s = ctx.gls_get_stats()
+        log(f"warmup {i}: kernel {s['kernel_ms']:.1f} ms, {s['gate_evals']} gate-evals, "
+            f"{s['out_transitions']} outputs, {s['chunks']} chunks, arena {s['arena_used_bytes'] / 1e9:.1f} GB "
+            f"(wall {time.perf_counter() - t:.2f}s)")
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kernel_ms = []
+    ev0.record(stream)
+    for _ in range(a.steps):
+        step()
+        kernel_ms.append(ctx.gls_get_stats()["kernel_ms"])
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    ck = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / a.steps
+    s = ctx.gls_get_stats()
+    units = s["gate_evals"]
+    outs = s["out_transitions"]
+    alg = s["alg_bytes"]
+    kms = statistics.mean(kernel_ms)
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([ms, kms, units, outs, alg], dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(tt) for _ in range(world)]
+        dist.all_gather(allv, tt)
+        allv = torch.stack(allv).cpu().numpy()
+        ms, kms = float(allv[:, 0].max()), float(allv[:, 1].max())
+        units, outs, alg = float(allv[:, 2].sum()), float(allv[:, 3].sum()), float(allv[:, 4].sum())
+
+    # e2e through the public API with host buffers (pinned), every step:
+    # H2D of the given waveforms, simulate, D2H of the per-net hashes
+    e2e = None
+    if not a.no_e2e:
+        h_off = torch.empty(d_off.numel(), dtype=torch.int64, pin_memory=True)
+        h_tr = torch.empty(n_in, dtype=torch.int64, pin_memory=True)
+        h_off.copy_(d_off)
+        h_tr.copy_(d_tr)
+        off_np, tr_np = h_off.numpy(), h_tr.numpy().view(np.uint64)
+        n_e2e = max(1, min(a.steps, 3))
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n_e2e):
+            ctx.gls_set_input_waveforms(nl.num_inputs, off_np, tr_np)
+            ctx.gls_simulate(duration)
+            hashes = ctx.gls_get_net_hashes()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e_ms = e0.elapsed_time(e1) / n_e2e
+        e_units = s["gate_evals"]
+        if world > 1:
+            import torch.distributed as dist
+            tt = torch.tensor([e_ms, e_units], dtype=torch.float64, device=dev)
+            allv = [torch.zeros_like(tt) for _ in range(world)]
+            dist.all_gather(allv, tt)
+            allv = torch.stack(allv).cpu().numpy()
+            e_ms, e_units = float(allv[:, 0].max()), float(allv[:, 1].sum())
+        e2e = {"value": e_units / (e_ms / 1e3), "unit": "gate-evals/s",
+               "h2d_bytes_per_step": int(8 * (d_off.numel() + n_in)),
+               "d2h_bytes_per_step": int(8 * hashes.size), "ms_per_step": e_ms,
+               "api": "gls_set_input_waveforms(host pinned) + gls_simulate + gls_get_net_hashes"}
+        del h_off, h_tr
+
+    # CPU oracle on a bounded prefix of the same workload + full-size parity there
+    cpu = parity = None
+    if rank == 0 and not a.no_cpu_baseline:
+        cyc = min(a.sample_cycles or SAMPLE_CYCLES[cfg], k_hi)
+        r, dt, tmax = oracle_sample(nl, spec, cyc)
+        cpu = {"value": r.gate_evals / dt, "unit": "gate-evals/s", "cores": 1, "kind": "oracle",
+               "sample": f"{cfg} netlist ({nl.num_gates} gates), first {cyc} of {nc} clock cycles "
+                         f"(t <= {tmax} ps): {r.gate_evals} gate-evals in {dt:.2f} s, single thread"}
+        gh = ctx.gls_get_net_hashes_window(0, tmax)
+        mism = int((gh != r.hashes).sum())
+        parity = {"window_ps": [0, tmax], "nets": int(gh.size), "hash_mismatches": mism,
+                  "bit_exact": mism == 0}
+        log(f"oracle sample: {r.gate_evals} gate-evals in {dt:.2f}s; parity mismatches {mism}")
+
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        achieved = alg / (kms / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
+        if os.path.exists(tp):
+            try:
+                with open(tp) as f:
+                    traffic = json.load(f).get(cfg)
+            except Exception:
+                traffic = None
+        line = {
+            "metric": "gate-evals/s", "value": units / (ms / 1e3), "unit": "gate-evals/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": cfg, "gates": nl.num_gates, "pis": nl.num_inputs, "pins": nl.num_pins,
+                       "levels": L, "duration_ps": spec.duration, "stimulus_transitions": n_in,
+                       "stimulus_wcv": round(wcv, 2), "halo_ps": H,
+                       "parallelism": f"time-windows x{world}" if world > 1 else "single GPU",
+                       "cache": "working set (given + computed waveforms) >> 126 MB L2; no flush needed"},
+            "output_transitions_per_s": outs / (ms / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "gls::sim_kernel", "kernel_ms": kms, "alg_bytes_per_launch": alg},
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+            "gpu_launches": 2 * a.steps,
+            "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    return run_gls(a)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

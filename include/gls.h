@@ -99,6 +99,7 @@ typedef struct gls_stats {
     int64_t alg_bytes;       /* algorithmic bytes of the gate-evaluation kernel
                                 (DESIGN.md §7): 8·Σ fan-in reads + 8·outputs +
                                 20·pins + 8·gates                                  */
+    int64_t fanin_reads;     /* Σ over pins of the driving net's transitions      */
     double kernel_ms;        /* CUDA-event time of the gate-evaluation kernel      */
     double simulate_ms;      /* CUDA-event time of the whole gls_simulate          */
 } gls_stats;
@@ -181,6 +182,10 @@ int gls_get_waveforms(gls_ctx *ctx, int64_t *offsets, uint64_t *transitions,
 int gls_get_net_hashes(gls_ctx *ctx, uint64_t *hashes);
 /* Same into a DEVICE array (for NCCL gathers). */
 int gls_get_net_hashes_device(gls_ctx *ctx, uint64_t *d_hashes);
+/* Same hash over only the transitions with t_lo <= t <= t_hi (host array, net
+ * order).  Used to verify time windows (multi-GPU sharding, sampled parity at
+ * full size).  GLS_EINVAL if t_hi < t_lo. */
+int gls_get_net_hashes_window(gls_ctx *ctx, int64_t t_lo, int64_t t_hi, uint64_t *hashes);
 /* Per-net transition counts, host int64 [num_inputs + num_gates]. */
 int gls_get_net_counts(gls_ctx *ctx, int64_t *counts);
 /* Counters and timings of the last gls_simulate. */

@@ -500,59 +500,15 @@ static int set_inputs_common(gls_ctx* ctx, int32_t P, int64_t total) {
     return GLS_OK;
 }
 
-int gls_set_input_waveforms(gls_ctx* ctx, int32_t P, const int64_t* offsets, const uint64_t* tr) {
-    if (!ctx) return GLS_EINVAL;
-    if (!offsets) return fail(ctx, GLS_EINVAL, "null offsets");
-    int rc = set_inputs_common(ctx, P, 0);
-    if (rc) return rc;
-    const int64_t total = offsets[P];
-    if (total < 0) return fail(ctx, GLS_EINVAL, "negative total");
-    if (offsets[0] != 0) return fail(ctx, GLS_EINVAL, "offsets[0] != 0");
-    if (total > 0 && !tr) return fail(ctx, GLS_EINVAL, "null transitions");
-    int64_t maxt = -1;
-    for (int32_t i = 0; i < P; ++i) {
-        if (offsets[i + 1] < offsets[i]) return fail(ctx, GLS_EINVAL, "offsets decrease at net %d", i);
-        int prev = GLS_VX;
-        int64_t pt = -1;
-        for (int64_t j = offsets[i]; j < offsets[i + 1]; ++j) {
-            int64_t t = GLS_TIME(tr[j]);
-            int v = GLS_VAL(tr[j]);
-            if (t >= (1ll << 61)) return fail(ctx, GLS_EINVAL, "net %d: time >= 2^61", i);
-            if (t <= pt) return fail(ctx, GLS_EINVAL, "net %d: times not strictly increasing at entry %lld", i, (long long)j);
-            if (v == prev) return fail(ctx, GLS_EINVAL, "net %d: value repeats the previous one at entry %lld", i, (long long)j);
-            prev = v;
-            pt = t;
-        }
-        maxt = std::max(maxt, pt);
-    }
+static int upload_and_validate(gls_ctx* ctx, int32_t P, const int64_t* off, const uint64_t* tr, int64_t total,
+                               cudaMemcpyKind kind) {
     ctx->has_inputs = ctx->has_result = false;
     ctx->in_total = total;
-    rc = ensure_arena(ctx, total + 1, false);
+    int rc = ensure_arena(ctx, total + 1, false);
     if (rc) return rc;
     CK(ctx->d_in_off.alloc(P + 1));
-    CK(cudaMemcpyAsync(ctx->d_in_off.p, offsets, sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, ctx->stream));
-    if (total)
-        CK(cudaMemcpyAsync(ctx->d_arena.p, tr, sizeof(uint64_t) * total, cudaMemcpyHostToDevice, ctx->stream));
-    CK(cudaStreamSynchronize(ctx->stream));
-    ctx->max_in_time = maxt;
-    ctx->has_inputs = true;
-    return GLS_OK;
-}
-
-int gls_set_input_waveforms_device(gls_ctx* ctx, int32_t P, const int64_t* d_off, const uint64_t* d_tr,
-                                   int64_t total) {
-    if (!ctx) return GLS_EINVAL;
-    int rc = set_inputs_common(ctx, P, total);
-    if (rc) return rc;
-    if (!d_off || (total > 0 && !d_tr)) return fail(ctx, GLS_EINVAL, "null device pointer");
-    ctx->has_inputs = ctx->has_result = false;
-    ctx->in_total = total;
-    rc = ensure_arena(ctx, total + 1, false);
-    if (rc) return rc;
-    CK(ctx->d_in_off.alloc(P + 1));
-    CK(cudaMemcpyAsync(ctx->d_in_off.p, d_off, sizeof(int64_t) * (P + 1), cudaMemcpyDeviceToDevice, ctx->stream));
-    if (total)
-        CK(cudaMemcpyAsync(ctx->d_arena.p, d_tr, sizeof(uint64_t) * total, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_in_off.p, off, sizeof(int64_t) * (P + 1), kind, ctx->stream));
+    if (total) CK(cudaMemcpyAsync(ctx->d_arena.p, tr, sizeof(uint64_t) * total, kind, ctx->stream));
     CK(cudaMemsetAsync(ctx->d_flag.p, 0, sizeof(unsigned) * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->d_flag64.p, 0, sizeof(unsigned long long) * 4, ctx->stream));
     CK(launch_validate_inputs(P, ctx->d_in_off.p, ctx->d_arena.p, total, ctx->d_flag.p, ctx->d_flag64.p, ctx->stream));
@@ -564,11 +520,37 @@ int gls_set_input_waveforms_device(gls_ctx* ctx, int32_t P, const int64_t* d_off
     CK(cudaMemcpyAsync(&last_off, ctx->d_in_off.p + P, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (err || last_off != total)
-        return fail(ctx, GLS_EINVAL, "device given waveforms invalid (flags %u, offsets[P]=%lld, total=%lld)", err,
-                    last_off, (long long)total);
+        return fail(ctx, GLS_EINVAL,
+                    "given waveforms invalid (%s%s%s)", (err & 1u) ? "bad offsets " : "",
+                    (err & 2u) ? "times not strictly increasing / value repeats the previous one (first X) / time >= 2^61 " : "",
+                    last_off != total ? "offsets[P] != total" : "");
     ctx->max_in_time = total ? (int64_t)mt : -1;
     ctx->has_inputs = true;
     return GLS_OK;
+}
+
+int gls_set_input_waveforms(gls_ctx* ctx, int32_t P, const int64_t* offsets, const uint64_t* tr) {
+    if (!ctx) return GLS_EINVAL;
+    if (!offsets) return fail(ctx, GLS_EINVAL, "null offsets");
+    int rc = set_inputs_common(ctx, P, 0);
+    if (rc) return rc;
+    const int64_t total = offsets[P];
+    if (offsets[0] != 0) return fail(ctx, GLS_EINVAL, "offsets[0] != 0");
+    for (int32_t i = 0; i < P; ++i)
+        if (offsets[i + 1] < offsets[i]) return fail(ctx, GLS_EINVAL, "offsets decrease at net %d", i);
+    if (total > 0 && !tr) return fail(ctx, GLS_EINVAL, "null transitions");
+    // one H2D of the packed CSR ("one round of data transfer"), then the
+    // per-transition rules are checked on the device
+    return upload_and_validate(ctx, P, offsets, tr, total, cudaMemcpyHostToDevice);
+}
+
+int gls_set_input_waveforms_device(gls_ctx* ctx, int32_t P, const int64_t* d_off, const uint64_t* d_tr,
+                                   int64_t total) {
+    if (!ctx) return GLS_EINVAL;
+    int rc = set_inputs_common(ctx, P, total);
+    if (rc) return rc;
+    if (!d_off || (total > 0 && !d_tr)) return fail(ctx, GLS_EINVAL, "null device pointer");
+    return upload_and_validate(ctx, P, d_off, d_tr, total, cudaMemcpyDeviceToDevice);
 }
 
 int gls_simulate(gls_ctx* ctx, int64_t duration) {
@@ -653,13 +635,7 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
         s.arena_used_bytes = (int64_t)c.arena_top * 8;
         s.kernel_ms = ms_k;
         s.simulate_ms = ms_s;
-        // algorithmic bytes (DESIGN.md §7): every fan-in waveform read once per pin
-        std::vector<unsigned long long> len((size_t)ctx->P + ctx->G);
-        if (!len.empty())
-            CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * len.size(), cudaMemcpyDeviceToHost));
-        long double reads = 0;
-        for (size_t n = 0; n < len.size(); ++n) reads += (long double)len[n] * (long double)ctx->net_fanout[n];
-        s.alg_bytes = (int64_t)(8.0L * reads + 8.0L * (long double)c.out_trans + 20.0L * ctx->E + 8.0L * ctx->G);
+        s.alg_bytes = -1;  // computed on demand by gls_get_stats
         ctx->has_result = true;
         return GLS_OK;
     }
@@ -669,6 +645,17 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
 int gls_get_stats(gls_ctx* ctx, gls_stats* out) {
     if (!ctx || !out) return GLS_EINVAL;
     if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    if (ctx->stats.alg_bytes < 0) {
+        // algorithmic bytes (DESIGN.md §7): every fan-in waveform read once per pin
+        std::vector<unsigned long long> len((size_t)ctx->P + ctx->G);
+        if (!len.empty())
+            CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * len.size(), cudaMemcpyDeviceToHost));
+        long double reads = 0;
+        for (size_t n = 0; n < len.size(); ++n) reads += (long double)len[n] * (long double)ctx->net_fanout[n];
+        ctx->stats.alg_bytes = (int64_t)(8.0L * reads + 8.0L * (long double)ctx->stats.out_transitions +
+                                         20.0L * ctx->E + 8.0L * ctx->G);
+        ctx->stats.fanin_reads = (int64_t)reads;
+    }
     *out = ctx->stats;
     return GLS_OK;
 }
@@ -746,6 +733,20 @@ int gls_get_net_hashes_device(gls_ctx* ctx, uint64_t* d_hashes) {
     cudaSetDevice(ctx->device);
     CK(launch_hashes(params(ctx), ctx->d_perm.p, d_hashes, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
+    return GLS_OK;
+}
+
+int gls_get_net_hashes_window(gls_ctx* ctx, int64_t t_lo, int64_t t_hi, uint64_t* hashes) {
+    if (!ctx || !hashes) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    if (t_hi < t_lo) return fail(ctx, GLS_EINVAL, "t_hi < t_lo");
+    const int64_t N = (int64_t)ctx->P + ctx->G;
+    DevBuf<uint64_t> d;
+    CK(d.alloc(N));
+    cudaSetDevice(ctx->device);
+    CK(launch_hashes_window(params(ctx), ctx->d_perm.p, t_lo, t_hi, d.p, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (N) CK(cudaMemcpy(hashes, d.p, sizeof(uint64_t) * N, cudaMemcpyDeviceToHost));
     return GLS_OK;
 }
 

@@ -93,5 +93,7 @@ int max_coresident_blocks(int device, int* per_sm);
 cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
                                    unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s);
 cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s);
+cudaError_t launch_hashes_window(const SimParams& p, const uint32_t* perm, long long t_lo, long long t_hi,
+                                 uint64_t* out, cudaStream_t s);
 
 }  // namespace gls

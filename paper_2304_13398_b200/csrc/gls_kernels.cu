@@ -23,6 +23,16 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
+    unsigned r;
+    asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // Device-wide barrier for a co-resident (cooperative) grid.  The last block to
 // arrive publishes the abort decision (any error raised before the barrier),
@@ -436,16 +446,17 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
             p.ck_off[id] = my;
             p.ck_cnt[id] = r.cnt;
             p.ck_vb[id] = (uint8_t)r.vb;
-            __threadfence();
-            unsigned prev = atomicAdd(&p.gate_done[gi], 1u);
+            // release (no L1 invalidation, unlike __threadfence): this chunk's
+            // descriptor is visible before the gate's done counter moves
+            const unsigned prev = atom_add_release(&p.gate_done[gi], 1u);
             if (prev == nch - 1) {
-                // last chunk of the gate: prefix counts + net length
-                __threadfence();
+                // last chunk of the gate: prefix counts + net length (strong loads
+                // read L2, never a stale L1 line)
                 const uint32_t base = p.net_ck[p.P + gi];
                 unsigned long long cum = 0;
                 for (uint32_t j = 0; j < nch; ++j) {
                     p.ck_cum[base + j] = cum;
-                    cum += __ldcg(&p.ck_cnt[base + j]);
+                    cum += ld_relaxed_u32(&p.ck_cnt[base + j]);
                 }
                 p.net_len[p.P + gi] = cum;
             }
@@ -462,7 +473,10 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
     }
 }
 
-__global__ void __launch_bounds__(kThreads) sim_kernel(SimParams p) {
+#ifndef GLS_MINB
+#define GLS_MINB 2
+#endif
+__global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
     __shared__ uint8_t s_lut[kLutBytes];
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) s_lut[i] = p.lut[i];
     __syncthreads();
@@ -542,6 +556,32 @@ __global__ void hash_kernel(SimParams p, const uint32_t* perm, uint64_t* out) {
     }
 }
 
+// per-net hash of the transitions with t_lo <= t <= t_hi (same definition)
+__global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long t_lo, long long t_hi, uint64_t* out) {
+    const int N = p.P + p.G;
+    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
+        uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
+        unsigned long long cnt = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            uint64_t h = splitmix64(0x9E3779B97F4A7C15ull ^ (uint64_t)cnt);
+            for (uint32_t j = cb; j < cb + nck; ++j) {
+                const uint64_t* s = p.arena + p.ck_off[j];
+                uint32_t c = p.ck_cnt[j];
+                if (c == 0 || etime(s[0]) > t_hi || etime(s[c - 1]) < t_lo) continue;
+                for (uint32_t q = 0; q < c; ++q) {
+                    long long t = etime(s[q]);
+                    if (t < t_lo || t > t_hi) continue;
+                    if (pass == 0) ++cnt; else h = splitmix64(h ^ s[q]);
+                }
+            }
+            if (pass == 1) {
+                int user = n < p.P ? n : p.P + (int)perm[n - p.P];
+                out[user] = h;
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------ launchers
 int max_coresident_blocks(int device, int* per_sm) {
     int nb = 0, sms = 0;
@@ -581,6 +621,16 @@ cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* ou
     int blocks = (N + 255) / 256;
     if (blocks > 8192) blocks = 8192;
     hash_kernel<<<blocks, 256, 0, s>>>(p, perm, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hashes_window(const SimParams& p, const uint32_t* perm, long long t_lo, long long t_hi,
+                                 uint64_t* out, cudaStream_t s) {
+    int N = p.P + p.G;
+    if (N == 0) return cudaSuccess;
+    int blocks = (N + 255) / 256;
+    if (blocks > 8192) blocks = 8192;
+    hash_window_kernel<<<blocks, 256, 0, s>>>(p, perm, t_lo, t_hi, out);
     return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgls.so")
+LIB_PATH = os.environ.get("GLS_LIB") or os.path.join(_HERE, "libgls.so")
 
 GLS_OK, GLS_EINVAL, GLS_ECYCLE, GLS_ENOMEM, GLS_ESTATE, GLS_ERANGE, GLS_ECUDA = 0, -1, -2, -3, -4, -5, -6
 STATUS = {0: "GLS_OK", -1: "GLS_EINVAL", -2: "GLS_ECYCLE", -3: "GLS_ENOMEM", -4: "GLS_ESTATE",
@@ -23,6 +23,7 @@ STATUS = {0: "GLS_OK", -1: "GLS_EINVAL", -2: "GLS_ECYCLE", -3: "GLS_ENOMEM", -4:
 EXPORTS = ["gls_create", "gls_destroy", "gls_last_error", "gls_version", "gls_set_config",
            "gls_load_netlist", "gls_set_input_waveforms", "gls_set_input_waveforms_device",
            "gls_simulate", "gls_get_waveforms", "gls_get_net_hashes", "gls_get_net_hashes_device",
+           "gls_get_net_hashes_window",
            "gls_get_net_counts", "gls_get_stats", "gls_get_halo", "gls_get_levels", "gls_lut_lookup"]
 
 
@@ -43,6 +44,7 @@ class gls_stats(ctypes.Structure):
                 ("out_transitions", ctypes.c_int64), ("chunks", ctypes.c_int64),
                 ("deep_chunks", ctypes.c_int64), ("levels", ctypes.c_int64),
                 ("arena_used_bytes", ctypes.c_int64), ("alg_bytes", ctypes.c_int64),
+                ("fanin_reads", ctypes.c_int64),
                 ("kernel_ms", ctypes.c_double), ("simulate_ms", ctypes.c_double)]
 
     def as_dict(self):
@@ -74,6 +76,7 @@ def load_library():
         "gls_get_waveforms": (ctypes.c_int, [vp, vp, vp, i64, p(i64)]),
         "gls_get_net_hashes": (ctypes.c_int, [vp, vp]),
         "gls_get_net_hashes_device": (ctypes.c_int, [vp, vp]),
+        "gls_get_net_hashes_window": (ctypes.c_int, [vp, i64, i64, vp]),
         "gls_get_net_counts": (ctypes.c_int, [vp, vp]),
         "gls_get_stats": (ctypes.c_int, [vp, p(gls_stats)]),
         "gls_get_halo": (ctypes.c_int, [vp, p(i64)]),
@@ -193,6 +196,11 @@ class Context:
     def gls_get_net_hashes(self) -> np.ndarray:
         h = np.zeros(self.num_inputs + self.num_gates, np.uint64)
         self._check(self._lib.gls_get_net_hashes(self._h, h.ctypes.data))
+        return h
+
+    def gls_get_net_hashes_window(self, t_lo, t_hi) -> np.ndarray:
+        h = np.zeros(self.num_inputs + self.num_gates, np.uint64)
+        self._check(self._lib.gls_get_net_hashes_window(self._h, int(t_lo), int(t_hi), h.ctypes.data))
         return h
 
     def gls_get_net_hashes_device(self, d_ptr):

@@ -204,8 +204,22 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
         cycle_hi = spec.ncycles
     counts = torch.zeros(P, dtype=torch.int64, device=dev)
     chunks = []
-    for p0 in range(0, P, pi_batch):
-        pis = torch.arange(p0, min(P, p0 + pi_batch), device=dev, dtype=torch.int64)
+    # batch PIs so that one batch covers at most ~`max_epochs` epochs (memory bound)
+    max_epochs = 1 << 26
+    allp = torch.arange(P, device=dev, dtype=torch.int64)
+    L_all, _, ph_all = _pi_params(spec, allp)
+    span = max(1, cycle_hi - cycle_lo)
+    ep = torch.div(torch.full_like(allp, span), L_all, rounding_mode="floor") + 2
+    cum = torch.cumsum(ep, 0).cpu().numpy()
+    bounds, p0 = [], 0
+    while p0 < P:
+        base = cum[p0 - 1] if p0 else 0
+        p1 = int(np.searchsorted(cum, base + max_epochs, side="right"))
+        p1 = min(P, max(p1, p0 + 1), p0 + pi_batch)
+        bounds.append((p0, p1))
+        p0 = p1
+    for p0, p1 in bounds:
+        pis = torch.arange(p0, p1, device=dev, dtype=torch.int64)
         L, off, phase = _pi_params(spec, pis)
         e_lo = _epoch_of_cycle(torch.full_like(pis, cycle_lo), L, phase)
         e_hi = _epoch_of_cycle(torch.full_like(pis, max(cycle_hi - 1, cycle_lo)), L, phase)
@@ -234,71 +248,40 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
     return offs, trans
 
 
-def stimuli_window(spec: StimSpec, t_clamp: int, t_hi: int) -> Stimuli:
-    """Given waveforms restricted to a window, for oracle samples (CPU).
-
-    Every transition with t_clamp < t <= t_hi is kept; all transitions at or
-    before t_clamp are collapsed into one transition AT t_clamp carrying the
-    value in effect there (omitted if that value is the initial X).  With
-    t_clamp < 0 this is the plain prefix [0, t_hi].  The halo argument that
-    makes such windows exact is DESIGN.md §4 (reading R17)."""
+def window_stimuli(spec: StimSpec, cycle_lo: int, cycle_hi: int, device="cpu", pi_batch=1 << 16):
+    """Given waveforms for the cycle window [cycle_lo, cycle_hi), for time-window
+    sharding and oracle samples.  Every transition of those cycles is kept; all
+    earlier transitions are collapsed into ONE transition at t_clamp =
+    cycle_lo * PERIOD carrying the value in effect there (omitted if it is the
+    initial X).  Transitions of cycle >= cycle_lo happen after t_clamp (offsets
+    >= 20 ps), so the result is a valid waveform set.  With cycle_lo = 0 it is
+    the plain prefix.  The halo argument that makes such windows exact is
+    DESIGN.md §4 (reading R17).  Returns torch (offsets, trans) on `device`."""
+    dev = torch.device(device)
     P = spec.num_inputs
-    k_hi = min(spec.ncycles, t_hi // PERIOD + 1)
-    if t_clamp < 0:
-        offs, tr = generate_stimuli(spec, "cpu", cycle_lo=0, cycle_hi=k_hi)
-        tr = tr.numpy().astype(np.uint64)
-        t = (tr >> np.uint64(2)).astype(np.int64)
-        keep = t <= t_hi
-        pi_of = np.repeat(np.arange(P), np.diff(offs.numpy()))
-        tr, pi_of = tr[keep], pi_of[keep]
-        counts = np.bincount(pi_of, minlength=P)
-        o = np.zeros(P + 1, np.int64)
-        o[1:] = np.cumsum(counts)
-        return Stimuli(o, tr)
-    # value at t_clamp: the level of the epoch holding the last transition <= t_clamp.
-    # The epoch of cycle k(t_clamp) may start at a cycle whose (jittered) time is
-    # after t_clamp, so look one cycle back as well.
-    k_c = max(0, t_clamp // PERIOD)
-    k_lo = max(0, k_c - 1)
-    offs, tr = generate_stimuli(spec, "cpu", cycle_lo=k_lo, cycle_hi=k_hi)
-    tr = tr.numpy().astype(np.uint64)
-    pi_of = np.repeat(np.arange(P), np.diff(offs.numpy()))
-    t = (tr >> np.uint64(2)).astype(np.int64)
-    v = (tr & np.uint64(3)).astype(np.int64)
-    pis = torch.arange(P, dtype=torch.int64)
-    L, off, phase = _pi_params(spec, pis)
-    # level in effect just before cycle k_lo's possible transition = level(epoch(k_lo - 1))
-    if k_lo > 0:
-        e_prev = _epoch_of_cycle(torch.full_like(pis, k_lo - 1), L, phase)
-        base = _level(spec, pis, e_prev).numpy()
-    else:
-        base = np.full(P, 2, np.int64)
-    val = base.copy()
-    before = t <= t_clamp
-    # the last transition at or before t_clamp per PI sets the value
-    idx = np.nonzero(before)[0]
-    if idx.size:
-        # entries are grouped by PI and time-ordered: keep each PI's last one
-        last = np.ones(idx.size, bool)
-        last[:-1] = pi_of[idx[:-1]] != pi_of[idx[1:]]
-        idx = idx[last]
-        val[pi_of[idx]] = v[idx]
-    after = ~before & (t <= t_hi)
-    waves_pi = pi_of[after]
-    waves_tr = tr[after]
-    has_clamp = val != 2
-    n_clamp = has_clamp.astype(np.int64)
-    counts = np.bincount(waves_pi, minlength=P) + n_clamp
-    o = np.zeros(P + 1, np.int64)
-    o[1:] = np.cumsum(counts)
-    out = np.zeros(int(o[-1]), np.uint64)
-    cl = np.nonzero(has_clamp)[0]
-    out[o[cl]] = (np.uint64(t_clamp) << np.uint64(2)) | val[cl].astype(np.uint64)
-    # scatter the in-window transitions after the clamp entries
-    start = o[:-1] + n_clamp
-    rank = np.arange(waves_pi.shape[0]) - np.searchsorted(waves_pi, waves_pi, side="left")
-    out[start[waves_pi] + rank] = waves_tr
-    return Stimuli(o, out)
+    offs, tr = generate_stimuli(spec, dev, pi_batch=pi_batch, cycle_lo=cycle_lo, cycle_hi=cycle_hi)
+    if cycle_lo <= 0:
+        return offs, tr
+    counts = offs[1:] - offs[:-1]
+    pis = torch.arange(P, device=dev, dtype=torch.int64)
+    L, _, phase = _pi_params(spec, pis)
+    lvl = _level(spec, pis, _epoch_of_cycle(torch.full_like(pis, cycle_lo - 1), L, phase))
+    has = lvl != 2
+    nc = has.to(torch.int64)
+    new_off = torch.zeros(P + 1, dtype=torch.int64, device=dev)
+    new_off[1:] = torch.cumsum(counts + nc, 0)
+    out = torch.empty(int(new_off[-1].item()), dtype=torch.int64, device=dev)
+    cl = torch.nonzero(has).flatten()
+    out[new_off[cl]] = (cycle_lo * PERIOD << 2) | lvl[cl]
+    if tr.numel():
+        pi_of = torch.repeat_interleave(pis, counts)
+        rank = torch.arange(tr.numel(), device=dev, dtype=torch.int64) - offs[pi_of]
+        out[new_off[pi_of] + nc[pi_of] + rank] = tr
+    return new_off, out
+
+
+def to_stimuli(offs, tr) -> Stimuli:
+    return Stimuli(offs.cpu().numpy().astype(np.int64), tr.cpu().numpy().astype(np.uint64))
 
 
 # --------------------------------------------------------------------------
