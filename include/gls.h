@@ -80,11 +80,14 @@ typedef struct gls_config {
                                 (one store); 0 = auto (most of the
                                 free HBM)                     */
     int64_t chunk_capacity;  /* max (gate, time-chunk) work items per run; 0 = auto */
-    int32_t chunk_events;    /* target merged input events per work item (M); 0 = 256 */
+    int32_t chunk_events;    /* target merged input events per work item (M);
+                                0 = 1024 (warp engine) / 256 (per-lane engine)   */
     int32_t blocks_per_sm;   /* persistent-kernel CTAs per SM; 0 = max co-resident */
     int32_t ring_limit;      /* TESTING: cap on the on-chip pending-schedule ring
                                 (1..32) to force the deep-backtrace path; 0 = 32 */
-    int32_t reserved[7];
+    int32_t engine;          /* 0 = warp-cooperative chunk evaluation (default),
+                                1 = one chunk per lane (reference engine for A/B)  */
+    int32_t reserved[6];
 } gls_config;
 
 typedef struct gls_stats {

@@ -221,7 +221,8 @@ SimParams params(gls_ctx* ctx) {
     p.deep_cap = ctx->d_deep.n;
     p.ctl = ctx->d_ctl.p;
     p.duration = ctx->duration;
-    p.M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : 256;
+    p.engine = ctx->cfg.engine == 1 ? 1 : 0;
+    p.M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : (p.engine == 0 ? 1024 : 256);
     int rl = ctx->cfg.ring_limit;
     p.ring_cap = (rl > 0 && rl < kRing) ? rl : kRing;
     return p;
@@ -229,7 +230,7 @@ SimParams params(gls_ctx* ctx) {
 
 // Chunk-table entries per arena entry for auto sizing.
 double chunk_ratio(gls_ctx* ctx) {
-    int M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : 256;
+    int M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : (ctx->cfg.engine == 1 ? 256 : 1024);
     double fan = (double)ctx->E / std::max<double>(1.0, (double)ctx->P + ctx->G);
     return 1.5 * (fan + 0.5) / (double)M;
 }
@@ -361,7 +362,7 @@ void gls_destroy(gls_ctx* ctx) {
 int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
     if (!ctx || !cfg) return GLS_EINVAL;
     if (cfg->arena_bytes < 0 || cfg->chunk_capacity < 0 || cfg->chunk_events < 0 || cfg->blocks_per_sm < 0 ||
-        cfg->ring_limit < 0 || cfg->ring_limit > kRing)
+        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 1)
         return fail(ctx, GLS_EINVAL, "invalid gls_config field");
     ctx->cfg = *cfg;
     return GLS_OK;
@@ -568,7 +569,7 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
     if (rc) return rc;
     if (!ctx->d_deep.p) CK(ctx->d_deep.alloc(std::max<int64_t>(1 << 20, std::min<int64_t>(16ll << 20, ctx->in_total))));
     int per_sm = 0;
-    int maxb = max_coresident_blocks(ctx->device, &per_sm);
+    int maxb = max_coresident_blocks(ctx->device, ctx->cfg.engine == 1 ? 1 : 0, &per_sm);
     int sms = per_sm ? maxb / per_sm : 0;
     int blocks = ctx->cfg.blocks_per_sm > 0 ? std::min(maxb, ctx->cfg.blocks_per_sm * sms) : maxb;
     if (blocks < 1) return fail(ctx, GLS_ECUDA, "simulation kernel cannot be resident (occupancy 0)");

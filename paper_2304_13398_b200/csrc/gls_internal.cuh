@@ -83,13 +83,14 @@ struct SimParams {
     long long duration;
     int32_t M;                  // target merged input events per chunk
     int32_t ring_cap;           // <= kRing
+    int32_t engine;             // 0 = warp-cooperative chunks, 1 = per-lane chunks
     uint32_t nblocks;
 };
 
 // kernels / launchers (gls_kernels.cu)
 cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaStream_t s);
 cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s);
-int max_coresident_blocks(int device, int* per_sm);
+int max_coresident_blocks(int device, int engine, int* per_sm);
 cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
                                    unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s);
 cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s);

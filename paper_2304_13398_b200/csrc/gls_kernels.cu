@@ -10,6 +10,8 @@
 // atomic page iterator of P:499 without page waste) and writes it.
 // DESIGN.md §4-§5 give the derivations; the kernel is checked bit-exactly
 // against oracle/ by tests/test_gpu_parity.py.
+#include <climits>
+
 #include "gls_internal.cuh"
 
 namespace gls {
@@ -174,7 +176,7 @@ __device__ unsigned long long window_bound(const SimParams& p, const ChunkSetup&
 // storage: a 32-entry ring in local memory, or a linear array in global
 // scratch sized by window_bound (exact for any backtrace depth, reading R13).
 template <bool WRITE, bool DEEP>
-__device__ void run_chunk(const SimParams& p, const ChunkSetup& s, const uint8_t* lut,
+__device__ __noinline__ void run_chunk(const SimParams& p, const ChunkSetup& s, const uint8_t* lut,
                           uint64_t* out, uint64_t* dbuf, unsigned long long dcap, ChunkOut& r) {
     uint64_t lring[DEEP ? 1 : kRing];
     uint64_t* ring = DEEP ? dbuf : lring;
@@ -473,11 +475,128 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
     }
 }
 
+// ------------------------------------------------------------------ warp engine
+}  // namespace gls
+#include "gls_warp.cuh"
+namespace gls {
+
+// The per-lane engine on one lane: count pass, exact allocation, write pass
+// (deep ring if the 32-entry ring overflows).  Used when a chunk defeats the
+// warp engine's bounded pending list.
+__device__ __noinline__ void lane_chunk(const SimParams& p, const ChunkSetup& s, const uint8_t* lut,
+                           unsigned long long& off, uint32_t& cnt, uint32_t& vb,
+                           unsigned long long& evals, unsigned long long& events, bool& fits) {
+    ChunkOut r{0, 0, 0, 2, false};
+    run_chunk<false, false>(p, s, lut, nullptr, nullptr, 0, r);
+    bool deep = false;
+    uint64_t* dbuf = nullptr;
+    unsigned long long dcap = 0;
+    if (r.overflow) {
+        deep = true;
+        dcap = window_bound(p, s);
+        const unsigned long long at = atomicAdd(&p.ctl->deep_top, dcap);
+        atomicAdd(&p.ctl->deep_chunks, 1ull);
+        if (at + dcap > p.deep_cap) {
+            atomicOr(&p.ctl->error, kErrDeep);
+            atomicMax(&p.ctl->need_deep, at + dcap);
+            fits = false;
+            cnt = 0;
+            return;
+        }
+        dbuf = p.deep + at;
+        run_chunk<false, true>(p, s, lut, nullptr, dbuf, dcap, r);
+        if (r.overflow) atomicOr(&p.ctl->error, kErrBug);
+    }
+    off = r.cnt ? atomicAdd(&p.ctl->arena_top, (unsigned long long)r.cnt) : 0ull;
+    fits = off + r.cnt <= p.arena_cap;
+    if (!fits) {
+        atomicOr(&p.ctl->error, kErrArena);
+        atomicMax(&p.ctl->need_arena, off + r.cnt);
+    } else {
+        ChunkOut r2{0, 0, 0, 2, false};
+        if (deep)
+            run_chunk<true, true>(p, s, lut, p.arena + off, dbuf, dcap, r2);
+        else
+            run_chunk<true, false>(p, s, lut, p.arena + off, nullptr, 0, r2);
+        if (r2.cnt != r.cnt) atomicOr(&p.ctl->error, kErrBug);
+    }
+    cnt = r.cnt;
+    vb = r.vb;
+    evals = r.evals;
+    events = r.events;
+}
+
+// record a finished chunk; the last chunk of its gate computes the net's prefix counts
+__device__ __forceinline__ void finish_chunk(const SimParams& p, unsigned long long id, const ChunkSetup& s,
+                                             uint32_t gi, uint32_t nch, unsigned long long off, uint32_t cnt,
+                                             uint32_t vb) {
+    p.ck_T[id] = s.T0;
+    p.ck_off[id] = off;
+    p.ck_cnt[id] = cnt;
+    p.ck_vb[id] = (uint8_t)vb;
+    const unsigned prev = atom_add_release(&p.gate_done[gi], 1u);
+    if (prev == nch - 1) {
+        const uint32_t base = p.net_ck[p.P + gi];
+        unsigned long long cum = 0;
+        for (uint32_t j = 0; j < nch; ++j) {
+            p.ck_cum[base + j] = cum;
+            cum += ld_relaxed_u32(&p.ck_cnt[base + j]);
+        }
+        p.net_len[p.P + gi] = cum;
+    }
+}
+
+// phase B with the warp engine: each warp takes one chunk at a time
+__device__ void process_level_warp(const SimParams& p, unsigned long long ck_begin, unsigned long long ck_end,
+                                   unsigned long long* work, const uint8_t* lut, wv::WS& ws) {
+    const unsigned lane = threadIdx.x & 31;
+    const unsigned long long n = ck_end - ck_begin;
+    for (;;) {
+        unsigned long long wb = 0;
+        if (lane == 0) wb = atomicAdd(work, 1ull);
+        wb = __shfl_sync(0xffffffffu, wb, 0);
+        if (wb >= n) break;
+        const unsigned long long id = ck_begin + wb;
+        ChunkSetup s;
+        uint32_t gi = 0, c = 0, nch = 1;
+        setup_chunk(p, id, s, gi, c, nch);
+        unsigned long long off = 0, ev = 0, evt = 0;
+        uint32_t cnt = 0, vb = 2;
+        bool fits = true;
+        const bool ok = wv::warp_chunk(p, ws, s, lut, off, cnt, vb, ev, evt, fits);
+        if (!ok) {
+            if (lane == 0) {
+                atomicAdd(&p.ctl->deep_chunks, 1ull);
+                lane_chunk(p, s, lut, off, cnt, vb, ev, evt, fits);
+            }
+            off = __shfl_sync(0xffffffffu, off, 0);
+            cnt = __shfl_sync(0xffffffffu, cnt, 0);
+            vb = __shfl_sync(0xffffffffu, vb, 0);
+            ev = __shfl_sync(0xffffffffu, ev, 0);
+            evt = __shfl_sync(0xffffffffu, evt, 0);
+            fits = __shfl_sync(0xffffffffu, (int)fits, 0) != 0;
+        } else {
+            ev = warp_sum64(ev);
+            evt = warp_sum64(evt);
+        }
+        if (lane == 0) {
+            if (fits) finish_chunk(p, id, s, gi, nch, off, cnt, vb);
+            atomicAdd(&p.ctl->gate_evals, ev);
+            atomicAdd(&p.ctl->events, evt);
+            atomicAdd(&p.ctl->out_trans, (unsigned long long)cnt);
+            atomicAdd(&p.ctl->chunks, 1ull);
+        }
+        __syncwarp();
+    }
+}
+
 #ifndef GLS_MINB
 #define GLS_MINB 2
 #endif
 __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
     __shared__ uint8_t s_lut[kLutBytes];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    wv::WS* s_ws = reinterpret_cast<wv::WS*>(s_dyn);
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) s_lut[i] = p.lut[i];
     __syncthreads();
     const unsigned warps_per_block = blockDim.x >> 5;
@@ -490,7 +609,10 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
         plan_level(p, l, gwarp, nwarps);
         if (grid_barrier(p.ctl, p.nblocks, gen)) return;
         const unsigned long long ck_end = *(volatile unsigned long long*)&p.ctl->chunk_top;
-        process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
+        if (p.engine == 0)
+            process_level_warp(p, ck_begin, ck_end, &p.work[l], s_lut, s_ws[threadIdx.x >> 5]);
+        else
+            process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
         if (grid_barrier(p.ctl, p.nblocks, gen)) return;
         ck_begin = ck_end;
     }
@@ -583,9 +705,12 @@ __global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long 
 }
 
 // ------------------------------------------------------------------ launchers
-int max_coresident_blocks(int device, int* per_sm) {
+static size_t dyn_smem(int engine) { return engine == 0 ? wv::kSmemBytes : 0; }
+
+int max_coresident_blocks(int device, int engine, int* per_sm) {
     int nb = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel, kThreads, 0);
+    cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wv::kSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel, kThreads, dyn_smem(engine));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm) *per_sm = nb;
     return nb * sms;
@@ -595,7 +720,7 @@ cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s) {
     SimParams q = p;
     q.nblocks = (uint32_t)blocks;
     void* args[] = {&q};
-    return cudaLaunchCooperativeKernel((void*)sim_kernel, dim3(blocks), dim3(kThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel((void*)sim_kernel, dim3(blocks), dim3(kThreads), args, dyn_smem(p.engine), s);
 }
 
 cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaStream_t s) {

@@ -36,7 +36,7 @@ class GlsError(RuntimeError):
 class gls_config(ctypes.Structure):
     _fields_ = [("arena_bytes", ctypes.c_int64), ("chunk_capacity", ctypes.c_int64),
                 ("chunk_events", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
-                ("ring_limit", ctypes.c_int32), ("reserved", ctypes.c_int32 * 7)]
+                ("ring_limit", ctypes.c_int32), ("engine", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
 class gls_stats(ctypes.Structure):
@@ -153,8 +153,9 @@ class Context:
         return self._lib.gls_last_error(self._h).decode()
 
     # ---- ABI calls ----------------------------------------------------------
-    def gls_set_config(self, arena_bytes=0, chunk_capacity=0, chunk_events=0, blocks_per_sm=0, ring_limit=0):
-        c = gls_config(arena_bytes, chunk_capacity, chunk_events, blocks_per_sm, ring_limit)
+    def gls_set_config(self, arena_bytes=0, chunk_capacity=0, chunk_events=0, blocks_per_sm=0, ring_limit=0,
+                       engine=0):
+        c = gls_config(arena_bytes, chunk_capacity, chunk_events, blocks_per_sm, ring_limit, engine)
         return self._check(self._lib.gls_set_config(self._h, ctypes.byref(c)))
 
     def gls_load_netlist(self, num_inputs, gate_type, fanin_offsets, fanin_net, pin_delay):

@@ -25,6 +25,9 @@ def run_oracle(nl, st, dur):
                            nl.pin_delay, st.offsets, st.trans, dur)
 
 
+ENGINES = [0, 1]   # 0 = warp-cooperative, 1 = per-lane
+
+
 def run_gpu(c, nl, st, dur, **cfg):
     c.gls_set_config(**cfg)
     c.load(nl)
@@ -49,16 +52,18 @@ def assert_same(c, nl, st, dur, ref=None, hashes=True, **cfg):
     return s
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("ex", golden_io.examples(), ids=lambda e: e.name)
-def test_worked_examples(ctx, ex):
+def test_worked_examples(ctx, ex, engine):
     nl, st, dur, index, exp = ex.build()
-    w, _ = run_gpu(ctx, nl, st, dur)
+    w, _ = run_gpu(ctx, nl, st, dur, engine=engine)
     for net, wave in exp.items():
         assert w.wave(net) == wave, (ex.name, nl.names[net])
-    assert_same(ctx, nl, st, dur)
+    assert_same(ctx, nl, st, dur, engine=engine)
 
 
-def test_random_designs_1000(ctx):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_random_designs_1000(ctx, engine):
     """SPEC-style acceptance: >= 1000 random designs."""
     rng = np.random.Generator(np.random.PCG64(2024))
     for d in range(1000):
@@ -68,59 +73,66 @@ def test_random_designs_1000(ctx):
         st = W.random_stimuli(d, P, int(rng.integers(0, 40)), 400, xz=float(rng.random() * 0.3),
                               max_gap=int(rng.integers(1, 30)))
         try:
-            assert_same(ctx, nl, st, 450, hashes=(d % 10 == 0))
+            assert_same(ctx, nl, st, 450, hashes=(d % 10 == 0), engine=engine)
         except AssertionError as e:
             raise AssertionError(f"design {d}: {e}")
 
 
-@pytest.mark.parametrize("M", [1, 2, 3, 5, 17])
-def test_small_chunks_exact(ctx, M):
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("M", [1, 2, 3, 5, 17, 300])
+def test_small_chunks_exact(ctx, M, engine):
     """Many (gate, time-chunk) items per gate: halo starts, chunk value-before
     and cross-chunk cursors all exercised."""
     for seed in range(15):
         nl = W.random_dag(500 + seed, 6, 80, max_delay=20)
         st = W.random_stimuli(seed, 6, 60, 3000, xz=0.1, max_gap=60)
-        assert_same(ctx, nl, st, 3100, chunk_events=M, hashes=False)
+        assert_same(ctx, nl, st, 3100, chunk_events=M, hashes=False, engine=engine)
 
 
 @pytest.mark.parametrize("ring", [1, 2, 3])
 def test_deep_backtrace_path(ctx, ring):
-    """Pending-schedule ring overflow -> exact deep path (reading R13)."""
+    """Pending-schedule ring overflow -> exact deep path (reading R13), per-lane engine."""
     deep = 0
     for seed in range(12):
         nl = W.random_dag(700 + seed, 5, 60, max_delay=40)
         st = W.random_stimuli(seed, 5, 80, 800, xz=0.2, max_gap=4)
-        s = assert_same(ctx, nl, st, 900, ring_limit=ring, chunk_events=int(8 + seed), hashes=False)
+        s = assert_same(ctx, nl, st, 900, ring_limit=ring, chunk_events=int(8 + seed), hashes=False, engine=1)
         deep += s["deep_chunks"]
     assert deep > 0
 
 
-def test_zero_and_huge_delays(ctx):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_zero_and_huge_delays(ctx, engine):
     for seed in range(10):
         nl = W.random_dag(800 + seed, 4, 50, max_delay=0)
         st = W.random_stimuli(seed, 4, 30, 200, xz=0.3)
-        assert_same(ctx, nl, st, 250, hashes=False)
+        assert_same(ctx, nl, st, 250, hashes=False, engine=engine)
     nl = W.random_dag(900, 4, 40, max_delay=10)
     nl.pin_delay[::3] = (1 << 31) - 1
     st = W.random_stimuli(9, 4, 30, 200)
-    assert_same(ctx, nl, st, 250)
-    assert_same(ctx, nl, st, (1 << 33))
+    assert_same(ctx, nl, st, 250, engine=engine)
+    assert_same(ctx, nl, st, (1 << 33), engine=engine)
 
 
-def test_large_times(ctx):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_large_times(ctx, engine):
     base = 1 << 59
     nl = W.random_dag(901, 3, 30, max_delay=50)
     waves = [[(base + 10 * j + p, (j + p) % 2) for j in range(20)] for p in range(3)]
     st = W.stimuli_from_lists(waves)
-    assert_same(ctx, nl, st, (1 << 61) - 1)
+    assert_same(ctx, nl, st, (1 << 61) - 1, engine=engine)
+    # sparse, far-apart transitions: tiles limited by the 2^28 ps key span
+    waves = [[(j * (1 << 29) + 7 * p, (j + p) % 2) for j in range(12)] for p in range(3)]
+    assert_same(ctx, nl, W.stimuli_from_lists(waves), 13 * (1 << 29), engine=engine)
 
 
-def test_empty_and_constant_inputs(ctx):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_empty_and_constant_inputs(ctx, engine):
     nl = W.random_dag(902, 4, 30, max_delay=5)
     st = W.stimuli_from_lists([[], [], [], []])
-    assert_same(ctx, nl, st, 100)
+    assert_same(ctx, nl, st, 100, engine=engine)
     st = W.stimuli_from_lists([[(0, 1)], [], [(5, 3)], [(0, 0), (7, 2)]])
-    assert_same(ctx, nl, st, 100)
+    assert_same(ctx, nl, st, 100, engine=engine)
     # PIs only
     nl0 = W.netlist_from_gates(2, [])
     st0 = W.stimuli_from_lists([[(1, 0)], [(2, 3), (4, 1)]])
@@ -128,12 +140,13 @@ def test_empty_and_constant_inputs(ctx):
     assert w.wave(1) == [(2, 3), (4, 1)] and s["gate_evals"] == 0
 
 
-def test_c7552_shaped(ctx):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_c7552_shaped(ctx, engine):
     nl = W.config_netlist("c7552")
     spec = W.config_stimspec("c7552")
     o, t = W.generate_stimuli(spec)
     st = W.Stimuli(o.numpy(), t.numpy().astype(np.uint64))
-    s = assert_same(ctx, nl, st, spec.duration)
+    s = assert_same(ctx, nl, st, spec.duration, engine=engine)
     assert s["gate_evals"] > 1_000_000
 
 
@@ -144,7 +157,8 @@ def test_determinism_and_launch_shapes(ctx):
     st = W.Stimuli(o.numpy(), t.numpy().astype(np.uint64))
     ref = run_oracle(nl, st, spec.duration)
     base = None
-    for cfg in [dict(), dict(blocks_per_sm=1), dict(chunk_events=32), dict(chunk_events=4096), dict()]:
+    for cfg in [dict(), dict(blocks_per_sm=1), dict(chunk_events=32), dict(chunk_events=4096), dict(engine=1),
+                dict(engine=1, chunk_events=64), dict()]:
         w, _ = run_gpu(ctx, nl, st, spec.duration, **cfg)
         assert np.array_equal(w.trans, ref.trans)
         if base is None:
@@ -221,3 +235,15 @@ def test_generator_cpu_equals_gpu():
     o1, t1 = W.generate_stimuli(spec, "cpu")
     o2, t2 = W.generate_stimuli(spec, "cuda")
     assert torch.equal(o1, o2.cpu()) and torch.equal(t1, t2.cpu())
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_warp_engine_deep_pending_and_spills(ctx, seed):
+    """Large delay spreads with dense events overflow the warp engine's pending
+    list (-> per-lane fallback); long single-chunk gates spill its output buffer."""
+    nl = W.random_dag(1200 + seed, 4, 40, max_delay=400, min_delay=0)
+    st = W.random_stimuli(seed, 4, 600, 3000, xz=0.05, min_gap=1, max_gap=3)
+    s = assert_same(ctx, nl, st, 4000, engine=0, chunk_events=1 << 20, hashes=False)
+    nl = W.random_dag(1300 + seed, 3, 30, max_delay=2, types=[W.BUF, W.NOT, W.XOR])
+    st = W.random_stimuli(seed, 3, 3000, 60000, xz=0.0, min_gap=5, max_gap=30)
+    assert_same(ctx, nl, st, 61000, engine=0, chunk_events=1 << 20, hashes=False)
