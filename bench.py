@@ -239,7 +239,8 @@ def run_gls(a):
         step()
         s = ctx.gls_get_stats()
         log(f"warmup {i}: kernel {s['kernel_ms']:.1f} ms, {s['gate_evals']} gate-evals, "
-            f"{s['out_transitions']} outputs, {s['chunks']} chunks, arena {s['arena_used_bytes'] / 1e9:.1f} GB "
+            f"{s['out_transitions']} outputs, {s['chunks']} chunks ({s['deep_chunks']} fallback), "
+            f"arena {s['arena_used_bytes'] / 1e9:.1f} GB "
             f"(wall {time.perf_counter() - t:.2f}s)")
     if world > 1:
         torch.distributed.barrier()

@@ -81,13 +81,21 @@ typedef struct gls_config {
                                 free HBM)                     */
     int64_t chunk_capacity;  /* max (gate, time-chunk) work items per run; 0 = auto */
     int32_t chunk_events;    /* target merged input events per work item (M);
-                                0 = 1024 (warp engine) / 256 (per-lane engine)   */
+                                0 = 4096 / 256 / 2048 for engines 0 / 1 / 2       */
     int32_t blocks_per_sm;   /* persistent-kernel CTAs per SM; 0 = max co-resident */
     int32_t ring_limit;      /* TESTING: cap on the on-chip pending-schedule ring
                                 (1..32) to force the deep-backtrace path; 0 = 32 */
-    int32_t engine;          /* 0 = warp-cooperative chunk evaluation (default),
-                                1 = one chunk per lane (reference engine for A/B)  */
-    int32_t reserved[6];
+    int32_t engine;          /* evaluation engine of a (gate, time-chunk) item:
+                                0 = lanes on balanced time slices of one chunk per warp (default),
+                                1 = one chunk per lane (reference engine for A/B),
+                                2 = warp-cooperative tiles (merge path + warp scans) */
+    int32_t scheduler;       /* 0 = dataflow: a gate is scheduled when its last fan-in
+                                gate completes (Alg. 1 unlock rule) (default);
+                                1 = topological levels separated by device barriers.
+                                Engine 1 always uses levels.                        */
+    int64_t deep_per_warp;   /* per-warp scratch (entries) for deep backtraces and
+                                output spills; 0 = 65536, grown automatically      */
+    int32_t reserved[2];
 } gls_config;
 
 typedef struct gls_stats {

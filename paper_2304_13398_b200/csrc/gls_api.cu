@@ -128,6 +128,8 @@ struct gls_ctx {
     std::vector<uint32_t> perm;        // internal gate -> user gate
     std::vector<uint32_t> inv;         // user gate -> internal gate
     std::vector<int64_t> net_fanout;   // internal net -> pins it drives
+    DevBuf<uint32_t> d_fo_off, d_fo_gate, d_pend0, d_pend;
+    DevBuf<unsigned long long> d_deep_wtop;
     DevBuf<int32_t> d_level_off;
     DevBuf<GateInfo> d_gate;
     DevBuf<uint32_t> d_pin_src;
@@ -152,6 +154,7 @@ struct gls_ctx {
     DevBuf<uint32_t> d_ck_cnt, d_ck_gate;
     DevBuf<uint8_t> d_ck_vb;
     DevBuf<uint64_t> d_deep;
+    DevBuf<uint64_t> d_wscr;
     DevBuf<Ctl> d_ctl;
     DevBuf<unsigned> d_flag;
     DevBuf<unsigned long long> d_flag64;
@@ -159,7 +162,9 @@ struct gls_ctx {
     // results
     bool has_result = false;
     int64_t duration = 0;
+    int64_t deep_per_warp = 0;
     Ctl last{};
+    unsigned long long last_chunk_top = 0;   // chunk ids used by earlier runs (cleared before the next)
     gls_stats stats{};
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
 };
@@ -193,6 +198,8 @@ int64_t free_bytes(gls_ctx* ctx) {
     return (int64_t)fr;
 }
 
+int default_M(int engine) { return engine == 0 ? 4096 : engine == 1 ? 256 : 2048; }
+
 SimParams params(gls_ctx* ctx) {
     SimParams p{};
     p.P = ctx->P;
@@ -218,11 +225,18 @@ SimParams params(gls_ctx* ctx) {
     p.gate_done = ctx->d_gate_done.p;
     p.work = ctx->d_work.p;
     p.deep = ctx->d_deep.p;
+    p.wscr = ctx->d_wscr.p;
+    p.deep_wtop = ctx->d_deep_wtop.p;
+    p.fo_off = ctx->d_fo_off.p;
+    p.fo_gate = ctx->d_fo_gate.p;
+    p.pend = ctx->d_pend.p;
     p.deep_cap = ctx->d_deep.n;
+    p.deep_per_warp = (unsigned long long)ctx->deep_per_warp;
     p.ctl = ctx->d_ctl.p;
     p.duration = ctx->duration;
-    p.engine = ctx->cfg.engine == 1 ? 1 : 0;
-    p.M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : (p.engine == 0 ? 1024 : 256);
+    p.engine = ctx->cfg.engine;
+    p.sched = (p.engine == 1 || ctx->cfg.scheduler == 1) ? 1 : 0;
+    p.M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : default_M(p.engine);
     int rl = ctx->cfg.ring_limit;
     p.ring_cap = (rl > 0 && rl < kRing) ? rl : kRing;
     return p;
@@ -230,7 +244,7 @@ SimParams params(gls_ctx* ctx) {
 
 // Chunk-table entries per arena entry for auto sizing.
 double chunk_ratio(gls_ctx* ctx) {
-    int M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : (ctx->cfg.engine == 1 ? 256 : 1024);
+    int M = ctx->cfg.chunk_events > 0 ? ctx->cfg.chunk_events : default_M(ctx->cfg.engine);
     double fan = (double)ctx->E / std::max<double>(1.0, (double)ctx->P + ctx->G);
     return 1.5 * (fan + 0.5) / (double)M;
 }
@@ -295,6 +309,7 @@ int ensure_chunks(gls_ctx* ctx, int64_t min_cap) {
     if (want >= (1ll << 32)) want = (1ll << 32) - 1;
     if ((int64_t)ctx->d_ck_T.n >= want) return GLS_OK;
     cudaError_t e;
+    ctx->last_chunk_top = 0;
     if ((e = ctx->d_ck_T.alloc(want)) != cudaSuccess || (e = ctx->d_ck_off.alloc(want)) != cudaSuccess ||
         (e = ctx->d_ck_cum.alloc(want)) != cudaSuccess || (e = ctx->d_ck_cnt.alloc(want)) != cudaSuccess ||
         (e = ctx->d_ck_gate.alloc(want)) != cudaSuccess || (e = ctx->d_ck_vb.alloc(want)) != cudaSuccess) {
@@ -362,7 +377,8 @@ void gls_destroy(gls_ctx* ctx) {
 int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
     if (!ctx || !cfg) return GLS_EINVAL;
     if (cfg->arena_bytes < 0 || cfg->chunk_capacity < 0 || cfg->chunk_events < 0 || cfg->blocks_per_sm < 0 ||
-        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 1)
+        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 2 ||
+        cfg->scheduler < 0 || cfg->scheduler > 1 || cfg->deep_per_warp < 0)
         return fail(ctx, GLS_EINVAL, "invalid gls_config field");
     ctx->cfg = *cfg;
     return GLS_OK;
@@ -460,6 +476,19 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
         arrive[P + i] = a + dmax;
         maxA = std::max(maxA, arrive[P + i]);
     }
+    // consumers of every internal net (gates only) and initial ready counters
+    std::vector<uint32_t> nfo_off((size_t)N + 1, 0), pend0((size_t)std::max<int32_t>(G, 1), 0);
+    for (uint32_t q = 0; q < (uint32_t)E; ++q) ++nfo_off[psrc[q] + 1];
+    for (int64_t n = 0; n < N; ++n) nfo_off[n + 1] += nfo_off[n];
+    std::vector<uint32_t> nfo_gate((size_t)std::max<int64_t>(E, 1));
+    {
+        std::vector<uint32_t> fill(nfo_off.begin(), nfo_off.end() - 1);
+        for (int32_t i = 0; i < G; ++i)
+            for (uint32_t q = ginfo[i].pin_off; q < ginfo[i].pin_off + ginfo[i].k; ++q) {
+                nfo_gate[fill[psrc[q]]++] = (uint32_t)i;
+                if (psrc[q] >= (uint32_t)P) ++pend0[i];
+            }
+    }
     // upload
     cudaSetDevice(ctx->device);
     ctx->has_netlist = ctx->has_inputs = ctx->has_result = false;
@@ -473,6 +502,13 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
     CK(ctx->d_net_len.alloc(N));
     CK(ctx->d_gate_done.alloc(G));
     CK(ctx->d_work.alloc(L + 1));
+    CK(ctx->d_fo_off.alloc(N + 1));
+    CK(ctx->d_fo_gate.alloc(std::max<int64_t>(E, 1)));
+    CK(ctx->d_pend0.alloc(G));
+    CK(ctx->d_pend.alloc(G));
+    CK(cudaMemcpy(ctx->d_fo_off.p, nfo_off.data(), sizeof(uint32_t) * (N + 1), cudaMemcpyHostToDevice));
+    if (E) CK(cudaMemcpy(ctx->d_fo_gate.p, nfo_gate.data(), sizeof(uint32_t) * E, cudaMemcpyHostToDevice));
+    if (G) CK(cudaMemcpy(ctx->d_pend0.p, pend0.data(), sizeof(uint32_t) * G, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->d_level_off.p, level_off.data(), sizeof(int32_t) * (L + 1), cudaMemcpyHostToDevice));
     if (G) {
         CK(cudaMemcpy(ctx->d_gate.p, ginfo.data(), sizeof(GateInfo) * G, cudaMemcpyHostToDevice));
@@ -567,21 +603,36 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
     ctx->duration = duration;
     int rc = ensure_chunks(ctx, 0);
     if (rc) return rc;
-    if (!ctx->d_deep.p) CK(ctx->d_deep.alloc(std::max<int64_t>(1 << 20, std::min<int64_t>(16ll << 20, ctx->in_total))));
     int per_sm = 0;
-    int maxb = max_coresident_blocks(ctx->device, ctx->cfg.engine == 1 ? 1 : 0, &per_sm);
+    const int sched = (ctx->cfg.engine == 1 || ctx->cfg.scheduler == 1) ? 1 : 0;
+    int maxb = max_coresident_blocks(ctx->device, ctx->cfg.engine, sched, &per_sm);
     int sms = per_sm ? maxb / per_sm : 0;
     int blocks = ctx->cfg.blocks_per_sm > 0 ? std::min(maxb, ctx->cfg.blocks_per_sm * sms) : maxb;
     if (blocks < 1) return fail(ctx, GLS_ECUDA, "simulation kernel cannot be resident (occupancy 0)");
+    if (ctx->d_wscr.n < warp_scratch_entries(blocks)) CK(ctx->d_wscr.alloc(warp_scratch_entries(blocks)));
+    const int64_t nwarps = (int64_t)blocks * (kThreads / 32);
+    if (ctx->deep_per_warp == 0) ctx->deep_per_warp = ctx->cfg.deep_per_warp > 0 ? ctx->cfg.deep_per_warp : (1 << 16);
+    if ((int64_t)ctx->d_deep.n < nwarps * ctx->deep_per_warp) CK(ctx->d_deep.alloc(nwarps * ctx->deep_per_warp));
+    if ((int64_t)ctx->d_deep_wtop.n < nwarps) CK(ctx->d_deep_wtop.alloc(nwarps));
 
     for (int attempt = 0; attempt < 3; ++attempt) {
         SimParams p = params(ctx);
         Ctl init{};
         init.chunk_top = (unsigned long long)ctx->P;
-        init.arena_top = (unsigned long long)ctx->in_total;
+        init.work_head = (unsigned long long)ctx->P;
+        init.arena_top = (unsigned long long)((ctx->in_total + 15) & ~15ll);   // 128-byte segments
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         CK(cudaMemcpyAsync(ctx->d_ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemsetAsync(ctx->d_work.p, 0, sizeof(unsigned long long) * (ctx->L + 1), ctx->stream));
+        if (ctx->G > 0) {
+            CK(cudaMemcpyAsync(ctx->d_pend.p, ctx->d_pend0.p, sizeof(uint32_t) * ctx->G, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+            // chunk ids not yet planned read as empty (0xffffffff): clear what the last run used
+            const size_t clear = ctx->last_chunk_top > 0
+                                     ? std::min<size_t>(ctx->d_ck_gate.n, (size_t)ctx->last_chunk_top)
+                                     : ctx->d_ck_gate.n;
+            CK(cudaMemsetAsync(ctx->d_ck_gate.p, 0xff, sizeof(uint32_t) * clear, ctx->stream));
+        }
         CK(launch_init_given(p, ctx->d_in_off.p, ctx->stream));
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (ctx->G > 0) CK(launch_simulate(p, blocks, ctx->stream));
@@ -589,13 +640,17 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
         CK(cudaMemcpyAsync(&ctx->last, ctx->d_ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         const Ctl& c = ctx->last;
+        ctx->last_chunk_top = std::max<unsigned long long>(c.chunk_top, ctx->last_chunk_top);
         if (c.error & kErrBug) return fail(ctx, GLS_ECUDA, "internal consistency check failed (pass counts differ)");
+        if (c.error & kErrWatchdog)
+            return fail(ctx, GLS_ECUDA, "dataflow scheduler watchdog: no gate completed for 10 s (%llu of %d done)",
+                        c.done_gates, ctx->G);
         if (c.error & (kErrArena | kErrChunks | kErrDeep)) {
             // grow what overflowed and retry (auto sizing), else report what is needed
             bool retried = false;
             if ((c.error & kErrDeep)) {
-                int64_t need = (int64_t)c.need_deep * 2;
-                CK(ctx->d_deep.alloc(need));
+                ctx->deep_per_warp = std::max<int64_t>(ctx->deep_per_warp * 2, (int64_t)c.need_deep * 2);
+                CK(ctx->d_deep.alloc(nwarps * ctx->deep_per_warp));
                 retried = true;
             }
             if ((c.error & kErrChunks)) {

@@ -35,13 +35,14 @@ struct GateInfo {
     uint8_t pad;
 };
 
-enum : unsigned { kErrArena = 1u, kErrChunks = 2u, kErrDeep = 4u, kErrInput = 8u, kErrBug = 16u };
+enum : unsigned { kErrArena = 1u, kErrChunks = 2u, kErrDeep = 4u, kErrInput = 8u, kErrBug = 16u, kErrWatchdog = 32u };
 
 // device control block, initialised by the host before each run
 struct Ctl {
     unsigned long long chunk_top;   // next free chunk id (starts at P: one chunk per given net)
     unsigned long long arena_top;   // next free arena entry (starts after the given waveforms)
-    unsigned long long deep_top;    // deep-backtrace scratch bump pointer (reset per level)
+    unsigned long long work_head;   // dataflow queue: next chunk id to hand out (starts at P)
+    unsigned long long done_gates;  // dataflow: completed gates
     unsigned int bar_count;
     unsigned int bar_gen;
     unsigned int bar_abort;
@@ -77,20 +78,28 @@ struct SimParams {
     unsigned long long ck_cap;
     uint32_t* gate_done;        // [G] finished chunks per gate
     unsigned long long* work;   // [L+1] per-level work counters
-    uint64_t* deep;             // deep-backtrace scratch
+    uint64_t* deep;             // deep-backtrace scratch: one region per warp
+    uint64_t* wscr;             // per-warp output scratch
     unsigned long long deep_cap;
+    unsigned long long deep_per_warp;
+    unsigned long long* deep_wtop;  // [warps] bump pointer of each warp's region
+    const uint32_t* fo_off;     // [P+G+1] consumers (internal gates) of each net
+    const uint32_t* fo_gate;    // [E_gate]
+    uint32_t* pend;             // [G] fan-in pins whose driver gate is not complete yet
     Ctl* ctl;
     long long duration;
     int32_t M;                  // target merged input events per chunk
     int32_t ring_cap;           // <= kRing
-    int32_t engine;             // 0 = warp-cooperative chunks, 1 = per-lane chunks
+    int32_t engine;             // 0 = lane slices, 1 = per-lane chunks, 2 = warp tiles
+    int32_t sched;              // 0 = dataflow (ready counters), 1 = level barriers
     uint32_t nblocks;
 };
 
 // kernels / launchers (gls_kernels.cu)
 cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaStream_t s);
 cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s);
-int max_coresident_blocks(int device, int engine, int* per_sm);
+size_t warp_scratch_entries(int blocks);
+int max_coresident_blocks(int device, int engine, int sched, int* per_sm);
 cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
                                    unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s);
 cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s);

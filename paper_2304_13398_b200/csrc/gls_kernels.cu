@@ -1,15 +1,23 @@
 // gls_kernels.cu — sm_100a kernels of the gate-level re-simulation hot path.
 //
-// One persistent cooperative kernel (sim_kernel) runs the whole netlist in one
-// pass with no host round trip (the paper's one-pass property):
-// for each topological level it (A) plans (gate, time-chunk) work items and
-// (B) evaluates them, separated by device-wide barriers.  Each work item runs
-// Algorithm 2 over its chunk of time with an exact halo, applies
-// the Eq. 1 glitch filter with a streaming-finality rule, counts,
-// allocates its exact output segment (warp-aggregated bump allocation, the
-// atomic page iterator of P:499 without page waste) and writes it.
-// DESIGN.md §4-§5 give the derivations; the kernel is checked bit-exactly
-// against oracle/ by tests/test_gpu_parity.py.
+// One persistent cooperative kernel (sim_kernel) evaluates the whole netlist in
+// one pass with no host round trip (the paper's one-pass property, P:100,
+// P:254).  Work items are (gate, time-chunk) pairs: Algorithm 2
+// over the chunk's time range with an exact halo, the Eq. 1 glitch filter
+// with a streaming-finality rule, and an exact output segment per
+// chunk (bump allocation without page waste, cf. the atomic page iterator of
+// P:499).  Two schedulers:
+//   * dataflow (default): Alg. 1's unlock rule on the device —
+//     a gate's chunks are planned and published the moment its last fan-in
+//     gate completes (per-gate ready counters); warps pull published chunks
+//     from one queue, so no warp ever waits for a level to drain;
+//   * level barriers: plan a topological level, device-wide barrier, evaluate
+//     it, barrier (kept for A/B and for the per-lane engine).
+// Three evaluation engines (gls_config.engine): 0 lanes on balanced time slices
+// of one chunk per warp (gls_slice.cuh), 1 one chunk per lane (below), 2
+// warp-cooperative tiles (gls_warp.cuh).  DESIGN.md §4-§5 give the derivations;
+// every engine / scheduler is checked bit-exactly against oracle/ by
+// tests/test_gpu_parity.py.
 #include <climits>
 
 #include "gls_internal.cuh"
@@ -35,6 +43,18 @@ __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// release fence without the L1 invalidation a full __threadfence() implies
+__device__ __forceinline__ void fence_release() { asm volatile("fence.release.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned warp_global_id() { return blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); }
 
 // Device-wide barrier for a co-resident (cooperative) grid.  The last block to
 // arrive publishes the abort decision (any error raised before the barrier),
@@ -75,6 +95,11 @@ __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
     for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
     return x;
 }
+__device__ __forceinline__ unsigned long long warp_max64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x = max(x, (unsigned long long)__shfl_xor_sync(0xffffffffu, x, o));
+    return x;
+}
 
 // Z is read as X: code 3 -> 2.
 __device__ __forceinline__ uint32_t norm_code(uint32_t v) { return v ^ ((v >> 1) & v & 1u); }
@@ -83,16 +108,52 @@ __device__ __forceinline__ uint32_t rank_code(uint32_t f) { return ((f & 1u) << 
 
 __device__ __forceinline__ long long etime(uint64_t e) { return (long long)(e >> 2); }
 
+// ------------------------------------------------------------------ allocation
+// Output segments start on 128-byte lines (16 entries): no L1 line ever mixes
+// a finished segment with one still being written, so reads of published
+// segments need no L1 invalidation (dataflow scheduler).
+constexpr unsigned long long kSegAlign = 16;
+__device__ __forceinline__ unsigned long long seg_round(unsigned long long n) {
+    return (n + kSegAlign - 1) & ~(kSegAlign - 1);
+}
+// whole warp: exact (rounded) space for `total` entries; ~0 on overflow (flag raised)
+__device__ unsigned long long arena_alloc(const SimParams& p, uint32_t total) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long at = 0;
+    if (lane == 0 && total) at = atomicAdd(&p.ctl->arena_top, seg_round(total));
+    at = __shfl_sync(0xffffffffu, at, 0);
+    if (at + total > p.arena_cap) {
+        if (lane == 0) {
+            atomicOr(&p.ctl->error, kErrArena);
+            atomicMax(&p.ctl->need_arena, at + total);
+        }
+        return ~0ull;
+    }
+    return at;
+}
+// one lane: space in this warp's private deep-scratch region (reset per chunk); ~0 on overflow
+__device__ unsigned long long deep_alloc(const SimParams& p, unsigned long long n) {
+    const unsigned w = warp_global_id();
+    const unsigned long long at = atomicAdd(&p.deep_wtop[w], n);
+    if (at + n > p.deep_per_warp) {
+        atomicOr(&p.ctl->error, kErrDeep);
+        atomicMax(&p.ctl->need_deep, at + n);
+        return ~0ull;
+    }
+    return (unsigned long long)w * p.deep_per_warp + at;
+}
+
+// ------------------------------------------------------------------ net access
 // time of the idx-th transition of a net (idx < net_len)
 __device__ long long time_at(const SimParams& p, uint32_t net, unsigned long long idx) {
-    uint32_t cb = p.net_ck[net], n = p.net_nck[net];
+    uint32_t cb = __ldcg(&p.net_ck[net]), n = __ldcg(&p.net_nck[net]);
     uint32_t lo = 0, hi = n;  // largest j with cum[cb+j] <= idx
     while (hi - lo > 1) {
         uint32_t mid = (lo + hi) >> 1;
-        if (p.ck_cum[cb + mid] <= idx) lo = mid; else hi = mid;
+        if (__ldcg(&p.ck_cum[cb + mid]) <= idx) lo = mid; else hi = mid;
     }
     uint32_t j = cb + lo;
-    return etime(p.arena[p.ck_off[j] + (idx - p.ck_cum[j])]);
+    return etime(p.arena[__ldcg(&p.ck_off[j]) + (idx - __ldcg(&p.ck_cum[j]))]);
 }
 
 // Cursor over one fan-in net's transitions (across its chunk segments).
@@ -105,8 +166,8 @@ struct Cursor {
 __device__ __forceinline__ void refill(const SimParams& p, Cursor& c) {
     while (c.ptr == c.end && c.ck + 1 < c.ck_end) {
         ++c.ck;
-        unsigned long long off = p.ck_off[c.ck];
-        uint32_t cnt = p.ck_cnt[c.ck];
+        unsigned long long off = __ldcg(&p.ck_off[c.ck]);
+        uint32_t cnt = __ldcg(&p.ck_cnt[c.ck]);
         c.ptr = p.arena + off;
         c.end = c.ptr + cnt;
     }
@@ -117,21 +178,21 @@ __device__ __forceinline__ uint64_t head(const Cursor& c) { return c.ptr < c.end
 // value at tau0 (X if none).  Uses the chunk start times and each chunk's
 // value-before (ck_vb) so no backward walk is needed.
 __device__ void locate(const SimParams& p, uint32_t net, long long tau0, Cursor& c, uint32_t& init) {
-    uint32_t cb = p.net_ck[net], n = p.net_nck[net];
+    uint32_t cb = __ldcg(&p.net_ck[net]), n = __ldcg(&p.net_nck[net]);
     uint32_t lo = 0, hi = n;  // largest j with ck_T[j] <= tau0 + 1 (default 0)
     while (hi - lo > 1) {
         uint32_t mid = (lo + hi) >> 1;
-        if (p.ck_T[cb + mid] <= tau0 + 1) lo = mid; else hi = mid;
+        if (__ldcg(&p.ck_T[cb + mid]) <= tau0 + 1) lo = mid; else hi = mid;
     }
     uint32_t j = cb + lo;
-    const uint64_t* seg = p.arena + p.ck_off[j];
-    uint32_t cnt = p.ck_cnt[j];
+    const uint64_t* seg = p.arena + __ldcg(&p.ck_off[j]);
+    uint32_t cnt = __ldcg(&p.ck_cnt[j]);
     uint32_t a = 0, b = cnt;  // first index with t > tau0
     while (a < b) {
         uint32_t m = (a + b) >> 1;
         if (etime(seg[m]) <= tau0) a = m + 1; else b = m;
     }
-    init = a > 0 ? (uint32_t)(seg[a - 1] & 3u) : (uint32_t)p.ck_vb[j];
+    init = a > 0 ? (uint32_t)(seg[a - 1] & 3u) : (uint32_t)__ldcg(&p.ck_vb[j]);
     c.ptr = seg + a;
     c.end = seg + cnt;
     c.ck = j;
@@ -142,7 +203,7 @@ __device__ void locate(const SimParams& p, uint32_t net, long long tau0, Cursor&
 struct ChunkSetup {
     uint32_t src[4];
     uint4 d[4];
-    uint32_t k, lut_base, dmin;
+    uint32_t k, lut_base, dmin, dmax;
     long long T0, T1, tau0;
 };
 
@@ -294,6 +355,7 @@ __device__ __noinline__ void run_chunk(const SimParams& p, const ChunkSetup& s, 
 // Plan level l: every gate gets ceil(n_in / M) chunks (n_in = Σ fan-in lengths,
 // at most len(ref)+1 where ref = longest fan-in); chunk ids are bump-allocated
 // per warp and each chunk records its gate.
+
 __device__ void plan_level(const SimParams& p, int l, unsigned gwarp, unsigned nwarps) {
     const unsigned lane = threadIdx.x & 31;
     const int g0 = p.level_off[l - 1], g1 = p.level_off[l];
@@ -344,14 +406,16 @@ __device__ void plan_level(const SimParams& p, int l, unsigned gwarp, unsigned n
 
 // ------------------------------------------------------------------ phase B
 __device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetup& s,
-                            uint32_t& g_out, uint32_t& c_out, uint32_t& nch_out) {
-    const uint32_t gi = p.ck_gate[id];
+                            uint32_t& g_out, uint32_t& c_out, uint32_t& nch_out,
+                            unsigned long long* q0_out = nullptr, unsigned long long* q1_out = nullptr,
+                            uint32_t* ref_out = nullptr, unsigned long long* nin_out = nullptr) {
+    const uint32_t gi = __ldcg(&p.ck_gate[id]);
     const GateInfo g = p.gate[gi];
-    const uint32_t base = p.net_ck[p.P + gi], nch = p.net_nck[p.P + gi];
+    const uint32_t base = __ldcg(&p.net_ck[p.P + gi]), nch = __ldcg(&p.net_nck[p.P + gi]);
     const uint32_t c = (uint32_t)(id - base);
     s.k = g.k;
     s.lut_base = g.lut_base;
-    unsigned long long lenref = 0;
+    unsigned long long lenref = 0, n_in = 0;
     uint32_t ref = 0;
     uint32_t dmin = 0xffffffffu, dmax = 0;
 #pragma unroll
@@ -363,7 +427,8 @@ __device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetu
             s.d[i] = d;
             dmin = min(dmin, min(min(d.x, d.y), min(d.z, d.w)));
             dmax = max(dmax, max(max(d.x, d.y), max(d.z, d.w)));
-            unsigned long long len = p.net_len[src];
+            unsigned long long len = __ldcg(&p.net_len[src]);
+            n_in += len;
             if (len > lenref) { lenref = len; ref = src; }
         } else {
             s.src[i] = 0;
@@ -371,14 +436,18 @@ __device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetu
         }
     }
     s.dmin = dmin;
+    s.dmax = dmax;
     // chunk boundaries: quantiles of the longest fan-in's transition times
-    auto bound = [&](uint32_t cc) -> long long {
+    auto qidx = [&](uint32_t cc) -> unsigned long long {
         unsigned long long q = lenref / nch, rm = lenref % nch;
-        unsigned long long idx = (unsigned long long)cc * q + ((unsigned long long)cc * rm) / nch;
-        return time_at(p, ref, idx);
+        return (unsigned long long)cc * q + ((unsigned long long)cc * rm) / nch;
     };
-    s.T0 = c == 0 ? 0 : bound(c);
-    s.T1 = c + 1 == nch ? p.duration + 1 : bound(c + 1);
+    s.T0 = c == 0 ? 0 : time_at(p, ref, qidx(c));
+    s.T1 = c + 1 == nch ? p.duration + 1 : time_at(p, ref, qidx(c + 1));
+    if (q0_out) *q0_out = qidx(c);
+    if (q1_out) *q1_out = c + 1 == nch ? lenref : qidx(c + 1);
+    if (ref_out) *ref_out = ref;
+    if (nin_out) *nin_out = n_in;
     // halo: H = dmax + 1 (reading R17 for one gate); tau0 may be negative
     s.tau0 = s.T0 - (long long)dmax - 1;
     g_out = gi;
@@ -391,6 +460,8 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
     const unsigned lane = threadIdx.x & 31;
     const unsigned long long n = ck_end - ck_begin;
     for (;;) {
+        if (lane == 0) p.deep_wtop[warp_global_id()] = 0;   // per-warp deep scratch, reused per batch
+        __syncwarp();
         unsigned long long wb = 0;
         if (lane == 0) wb = atomicAdd(work, 32ull);
         wb = __shfl_sync(0xffffffffu, wb, 0);
@@ -411,11 +482,9 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
                 // deep backtrace: exact path with a scratch ring sized by the window
                 deep = true;
                 dcap = window_bound(p, s);
-                unsigned long long at = atomicAdd(&p.ctl->deep_top, dcap);
+                const unsigned long long at = deep_alloc(p, dcap);
                 atomicAdd(&p.ctl->deep_chunks, 1ull);
-                if (at + dcap > p.deep_cap) {
-                    atomicOr(&p.ctl->error, kErrDeep);
-                    atomicMax(&p.ctl->need_deep, at + dcap);
+                if (at == ~0ull) {
                     deep = false;
                     r.cnt = 0;
                 } else {
@@ -454,7 +523,7 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
             if (prev == nch - 1) {
                 // last chunk of the gate: prefix counts + net length (strong loads
                 // read L2, never a stale L1 line)
-                const uint32_t base = p.net_ck[p.P + gi];
+                const uint32_t base = __ldcg(&p.net_ck[p.P + gi]);
                 unsigned long long cum = 0;
                 for (uint32_t j = 0; j < nch; ++j) {
                     p.ck_cum[base + j] = cum;
@@ -475,17 +544,21 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
     }
 }
 
-// ------------------------------------------------------------------ warp engine
-}  // namespace gls
-#include "gls_warp.cuh"
-namespace gls {
+// ------------------------------------------------------------------ chunk results, gates, dataflow
+struct ChunkResult {
+    ChunkSetup s;
+    uint32_t gi, nch;
+    unsigned long long off, evals, events;
+    uint32_t total, vb;
+    bool fits;
+};
 
 // The per-lane engine on one lane: count pass, exact allocation, write pass
-// (deep ring if the 32-entry ring overflows).  Used when a chunk defeats the
-// warp engine's bounded pending list.
+// (deep ring if the 32-entry ring overflows).  Used when a chunk defeats an
+// engine's bounded on-chip state.
 __device__ __noinline__ void lane_chunk(const SimParams& p, const ChunkSetup& s, const uint8_t* lut,
-                           unsigned long long& off, uint32_t& cnt, uint32_t& vb,
-                           unsigned long long& evals, unsigned long long& events, bool& fits) {
+                                        unsigned long long& off, uint32_t& cnt, uint32_t& vb,
+                                        unsigned long long& evals, unsigned long long& events, bool& fits) {
     ChunkOut r{0, 0, 0, 2, false};
     run_chunk<false, false>(p, s, lut, nullptr, nullptr, 0, r);
     bool deep = false;
@@ -494,11 +567,8 @@ __device__ __noinline__ void lane_chunk(const SimParams& p, const ChunkSetup& s,
     if (r.overflow) {
         deep = true;
         dcap = window_bound(p, s);
-        const unsigned long long at = atomicAdd(&p.ctl->deep_top, dcap);
-        atomicAdd(&p.ctl->deep_chunks, 1ull);
-        if (at + dcap > p.deep_cap) {
-            atomicOr(&p.ctl->error, kErrDeep);
-            atomicMax(&p.ctl->need_deep, at + dcap);
+        const unsigned long long at = deep_alloc(p, dcap);
+        if (at == ~0ull) {
             fits = false;
             cnt = 0;
             return;
@@ -507,7 +577,7 @@ __device__ __noinline__ void lane_chunk(const SimParams& p, const ChunkSetup& s,
         run_chunk<false, true>(p, s, lut, nullptr, dbuf, dcap, r);
         if (r.overflow) atomicOr(&p.ctl->error, kErrBug);
     }
-    off = r.cnt ? atomicAdd(&p.ctl->arena_top, (unsigned long long)r.cnt) : 0ull;
+    off = r.cnt ? atomicAdd(&p.ctl->arena_top, seg_round(r.cnt)) : 0ull;
     fits = off + r.cnt <= p.arena_cap;
     if (!fits) {
         atomicOr(&p.ctl->error, kErrArena);
@@ -526,95 +596,240 @@ __device__ __noinline__ void lane_chunk(const SimParams& p, const ChunkSetup& s,
     events = r.events;
 }
 
-// record a finished chunk; the last chunk of its gate computes the net's prefix counts
-__device__ __forceinline__ void finish_chunk(const SimParams& p, unsigned long long id, const ChunkSetup& s,
-                                             uint32_t gi, uint32_t nch, unsigned long long off, uint32_t cnt,
-                                             uint32_t vb) {
-    p.ck_T[id] = s.T0;
-    p.ck_off[id] = off;
-    p.ck_cnt[id] = cnt;
-    p.ck_vb[id] = (uint8_t)vb;
-    const unsigned prev = atom_add_release(&p.gate_done[gi], 1u);
-    if (prev == nch - 1) {
-        const uint32_t base = p.net_ck[p.P + gi];
-        unsigned long long cum = 0;
-        for (uint32_t j = 0; j < nch; ++j) {
-            p.ck_cum[base + j] = cum;
-            cum += ld_relaxed_u32(&p.ck_cnt[base + j]);
+// Whole warp: make gate c schedulable — nch = ceil(n_in / M) chunks (at most
+// len(longest fan-in) + 1), chunk ids from the shared queue, chunk -> gate map
+// written last (publication; consumers spin on it).
+__device__ void plan_gate(const SimParams& p, uint32_t c) {
+    const int lane = threadIdx.x & 31;
+    const GateInfo g = p.gate[c];
+    const unsigned long long len = (uint32_t)lane < g.k ? __ldcg(&p.net_len[p.pin_src[g.pin_off + lane]]) : 0ull;
+    const unsigned long long n_in = warp_sum64(len), lenref = warp_max64(len);
+    unsigned long long nch = (n_in + (unsigned long long)p.M - 1) / (unsigned long long)p.M;
+    if (nch < 1) nch = 1;
+    if (nch > lenref + 1) nch = lenref + 1;
+    unsigned long long base = 0;
+    if (lane == 0) base = atomicAdd(&p.ctl->chunk_top, nch);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base + nch > p.ck_cap) {
+        if (lane == 0) {
+            atomicOr(&p.ctl->error, kErrChunks);
+            atomicMax(&p.ctl->need_chunks, base + nch);
         }
-        p.net_len[p.P + gi] = cum;
+        return;
     }
+    if (lane == 0) {
+        p.net_ck[p.P + c] = (uint32_t)base;
+        p.net_nck[p.P + c] = (uint32_t)nch;
+        p.gate_done[c] = 0;
+        fence_release();
+    }
+    __syncwarp();
+    for (unsigned long long j = lane; j < nch; j += 32) st_relaxed_u32(&p.ck_gate[base + j], c);
 }
 
-// phase B with the warp engine: each warp takes one chunk at a time
-__device__ void process_level_warp(const SimParams& p, unsigned long long ck_begin, unsigned long long ck_end,
-                                   unsigned long long* work, const uint8_t* lut, wv::WS& ws) {
-    const unsigned lane = threadIdx.x & 31;
-    const unsigned long long n = ck_end - ck_begin;
-    for (;;) {
-        unsigned long long wb = 0;
-        if (lane == 0) wb = atomicAdd(work, 1ull);
-        wb = __shfl_sync(0xffffffffu, wb, 0);
-        if (wb >= n) break;
-        const unsigned long long id = ck_begin + wb;
-        ChunkSetup s;
-        uint32_t gi = 0, c = 0, nch = 1;
-        setup_chunk(p, id, s, gi, c, nch);
-        unsigned long long off = 0, ev = 0, evt = 0;
-        uint32_t cnt = 0, vb = 2;
-        bool fits = true;
-        const bool ok = wv::warp_chunk(p, ws, s, lut, off, cnt, vb, ev, evt, fits);
-        if (!ok) {
-            if (lane == 0) {
-                atomicAdd(&p.ctl->deep_chunks, 1ull);
-                lane_chunk(p, s, lut, off, cnt, vb, ev, evt, fits);
-            }
-            off = __shfl_sync(0xffffffffu, off, 0);
-            cnt = __shfl_sync(0xffffffffu, cnt, 0);
-            vb = __shfl_sync(0xffffffffu, vb, 0);
-            ev = __shfl_sync(0xffffffffu, ev, 0);
-            evt = __shfl_sync(0xffffffffu, evt, 0);
-            fits = __shfl_sync(0xffffffffu, (int)fits, 0) != 0;
-        } else {
-            ev = warp_sum64(ev);
-            evt = warp_sum64(evt);
+// Whole warp: the last chunk of gate gi finished — prefix counts, net length,
+// and (dataflow) unlock the consumers whose last fan-in this was (Alg. 1).
+template <bool DATAFLOW>
+__device__ void gate_complete(const SimParams& p, uint32_t gi, uint32_t base, uint32_t nch) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long cum = 0;
+    for (uint32_t j0 = 0; j0 < nch; j0 += 32) {
+        const uint32_t j = j0 + lane;
+        const unsigned long long c = j < nch ? ld_relaxed_u32(&p.ck_cnt[base + j]) : 0ull;
+        unsigned long long x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
         }
-        if (lane == 0) {
-            if (fits) finish_chunk(p, id, s, gi, nch, off, cnt, vb);
-            atomicAdd(&p.ctl->gate_evals, ev);
-            atomicAdd(&p.ctl->events, evt);
-            atomicAdd(&p.ctl->out_trans, (unsigned long long)cnt);
-            atomicAdd(&p.ctl->chunks, 1ull);
-        }
-        __syncwarp();
+        if (j < nch) p.ck_cum[base + j] = cum + x - c;
+        cum += __shfl_sync(0xffffffffu, x, 31);
     }
+    if (lane == 0) p.net_len[p.P + gi] = cum;
+    if (!DATAFLOW) return;
+    fence_release();
+    __syncwarp();
+    const uint32_t net = (uint32_t)p.P + gi;
+    const uint32_t f0 = p.fo_off[net], f1 = p.fo_off[net + 1];
+    for (uint32_t e0 = f0; e0 < f1; e0 += 32) {
+        const uint32_t e = e0 + (uint32_t)lane;
+        uint32_t cg = 0;
+        bool ready = false;
+        if (e < f1) {
+            cg = p.fo_gate[e];
+            ready = atom_add_release(&p.pend[cg], 0xffffffffu) == 1u;   // decrement
+        }
+        for (unsigned rb = __ballot_sync(0xffffffffu, ready); rb; rb &= rb - 1) {
+            const int src = __ffs(rb) - 1;
+            plan_gate(p, __shfl_sync(0xffffffffu, cg, src));
+        }
+    }
+    __syncwarp();
+    if (lane == 0) atomicAdd(&p.ctl->done_gates, 1ull);
 }
+
+// Whole warp: record a finished chunk (descriptor, stats); the gate's last
+// chunk completes the gate.
+template <bool DATAFLOW>
+__device__ void chunk_done(const SimParams& p, unsigned long long id, const ChunkResult& R) {
+    const int lane = threadIdx.x & 31;
+    unsigned prev = 0;
+    if (lane == 0) {
+        if (R.fits) {
+            p.ck_T[id] = R.s.T0;
+            p.ck_off[id] = R.off;
+            p.ck_cnt[id] = R.total;
+            p.ck_vb[id] = (uint8_t)R.vb;
+            prev = atom_add_release(&p.gate_done[R.gi], 1u);
+        }
+        atomicAdd(&p.ctl->gate_evals, R.evals);
+        atomicAdd(&p.ctl->events, R.events);
+        atomicAdd(&p.ctl->out_trans, (unsigned long long)R.total);
+        atomicAdd(&p.ctl->chunks, 1ull);
+    }
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (R.fits && prev == R.nch - 1)
+        gate_complete<DATAFLOW>(p, R.gi, __ldcg(&p.net_ck[p.P + R.gi]), R.nch);
+    __syncwarp();
+}
+
+
+}  // namespace gls
+#include "gls_warp.cuh"
+namespace gls {
+
+// one chunk with the warp-cooperative tile engine (whole warp)
+__device__ void process_chunk_warp(const SimParams& p, unsigned long long id, const uint8_t* lut, wv::WS& ws,
+                                   ChunkResult& R) {
+    const int lane = threadIdx.x & 31;
+    uint32_t c = 0;
+    setup_chunk(p, id, R.s, R.gi, c, R.nch);
+    uint64_t* scr = p.wscr + (size_t)warp_global_id() * wv::OBG;
+    unsigned long long off = 0, ev = 0, evt = 0;
+    uint32_t cnt = 0, vb = 2;
+    bool fits = true;
+    const bool ok = wv::warp_chunk(p, ws, scr, R.s, lut, off, cnt, vb, ev, evt, fits);
+    if (!ok) {
+        if (lane == 0) {
+            atomicAdd(&p.ctl->deep_chunks, 1ull);
+            lane_chunk(p, R.s, lut, off, cnt, vb, ev, evt, fits);
+        }
+        off = __shfl_sync(0xffffffffu, off, 0);
+        cnt = __shfl_sync(0xffffffffu, cnt, 0);
+        vb = __shfl_sync(0xffffffffu, vb, 0);
+        ev = __shfl_sync(0xffffffffu, ev, 0);
+        evt = __shfl_sync(0xffffffffu, evt, 0);
+        fits = __shfl_sync(0xffffffffu, (int)fits, 0) != 0;
+    } else {
+        ev = warp_sum64(ev);
+        evt = warp_sum64(evt);
+    }
+    R.off = off;
+    R.total = cnt;
+    R.vb = vb;
+    R.evals = ev;
+    R.events = evt;
+    R.fits = fits;
+}
+
+}  // namespace gls
+#include "gls_slice.cuh"
+namespace gls {
 
 #ifndef GLS_MINB
 #define GLS_MINB 2
 #endif
+constexpr int kDtabWords = 24;   // per-thread delay table words (slice engine)
+constexpr unsigned kEmpty = 0xffffffffu;
+
+template <int ENGINE>
+__device__ __forceinline__ void process_one(const SimParams& p, unsigned long long id, const uint8_t* lut,
+                                            unsigned char* s_dyn, ChunkResult& R) {
+    if (ENGINE == 0)
+        sl::process_chunk_slice(p, id, lut, reinterpret_cast<uint32_t*>(s_dyn), R);
+    else
+        process_chunk_warp(p, id, lut, reinterpret_cast<wv::WS*>(s_dyn)[threadIdx.x >> 5], R);
+}
+
+template <int ENGINE, bool DATAFLOW>
 __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
     __shared__ uint8_t s_lut[kLutBytes];
     extern __shared__ __align__(16) unsigned char s_dyn[];
-    wv::WS* s_ws = reinterpret_cast<wv::WS*>(s_dyn);
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) s_lut[i] = p.lut[i];
     __syncthreads();
+    const int lane = threadIdx.x & 31;
     const unsigned warps_per_block = blockDim.x >> 5;
     const unsigned gwarp = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
     const unsigned nwarps = gridDim.x * warps_per_block;
-    unsigned gen = 0;
-    unsigned long long ck_begin = (unsigned long long)p.P;
-    for (int l = 1; l <= p.L; ++l) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) p.ctl->deep_top = 0;
-        plan_level(p, l, gwarp, nwarps);
-        if (grid_barrier(p.ctl, p.nblocks, gen)) return;
-        const unsigned long long ck_end = *(volatile unsigned long long*)&p.ctl->chunk_top;
-        if (p.engine == 0)
-            process_level_warp(p, ck_begin, ck_end, &p.work[l], s_lut, s_ws[threadIdx.x >> 5]);
-        else
-            process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
-        if (grid_barrier(p.ctl, p.nblocks, gen)) return;
-        ck_begin = ck_end;
+    if (DATAFLOW) {
+        // seed: gates fed only by given nets (topological level 1) are ready now
+        for (int g = (int)gwarp; g < p.level_off[1]; g += (int)nwarps) plan_gate(p, (uint32_t)g);
+        // pull published chunks until every gate is complete (Alg. 1 loop)
+        for (;;) {
+            unsigned long long id = 0;
+            unsigned g = kEmpty;
+            if (lane == 0) {
+                id = atomicAdd(&p.ctl->work_head, 1ull);
+                unsigned ns = 32;
+                unsigned long long t_start = 0, seen = ~0ull;
+                for (;;) {
+                    if (id < p.ck_cap) {
+                        g = ld_relaxed_u32(&p.ck_gate[id]);
+                        if (g != kEmpty) break;
+                    }
+                    const unsigned long long done = ld_relaxed_u64(&p.ctl->done_gates);
+                    if (done >= (unsigned long long)p.G || ld_relaxed_u32(&p.ctl->error) != 0u) break;
+                    // watchdog: no gate completed anywhere for 10 s -> report instead of hanging
+                    unsigned long long now;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                    if (done != seen) {
+                        seen = done;
+                        t_start = now;
+                    } else if (now - t_start > 10000000000ull) {
+                        atomicOr(&p.ctl->error, kErrWatchdog);
+                        break;
+                    }
+                    __nanosleep(ns);
+                    if (ns < 1024) ns <<= 1;
+                }
+                p.deep_wtop[gwarp] = 0;                 // this warp's deep scratch, reused per chunk
+            }
+            g = __shfl_sync(0xffffffffu, g, 0);
+            id = __shfl_sync(0xffffffffu, id, 0);
+            if (g == kEmpty) return;
+            __syncwarp();
+            ChunkResult R;
+            process_one<ENGINE>(p, id, s_lut, s_dyn, R);
+            chunk_done<true>(p, id, R);
+        }
+    } else {
+        unsigned gen = 0;
+        unsigned long long ck_begin = (unsigned long long)p.P;
+        for (int l = 1; l <= p.L; ++l) {
+            plan_level(p, l, gwarp, nwarps);
+            if (grid_barrier(p.ctl, p.nblocks, gen)) return;
+            const unsigned long long ck_end = *(volatile unsigned long long*)&p.ctl->chunk_top;
+            if (ENGINE == 1) {
+                process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
+            } else {
+                const unsigned long long n = ck_end - ck_begin;
+                for (;;) {
+                    unsigned long long wb = 0;
+                    if (lane == 0) {
+                        wb = atomicAdd(&p.work[l], 1ull);
+                        p.deep_wtop[gwarp] = 0;
+                    }
+                    wb = __shfl_sync(0xffffffffu, wb, 0);
+                    if (wb >= n) break;
+                    __syncwarp();
+                    ChunkResult R;
+                    process_one<ENGINE>(p, ck_begin + wb, s_lut, s_dyn, R);
+                    chunk_done<false>(p, ck_begin + wb, R);
+                }
+            }
+            if (grid_barrier(p.ctl, p.nblocks, gen)) return;
+            ck_begin = ck_end;
+        }
     }
 }
 
@@ -705,12 +920,24 @@ __global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long 
 }
 
 // ------------------------------------------------------------------ launchers
-static size_t dyn_smem(int engine) { return engine == 0 ? wv::kSmemBytes : 0; }
+static size_t dyn_smem(int engine) {
+    return engine == 2 ? wv::kSmemBytes : (engine == 0 ? (size_t)kDtabWords * kThreads * 4 : 0);
+}
+static const void* kernel_for(int engine, int sched) {
+    if (engine == 1) return (const void*)sim_kernel<1, false>;
+    if (engine == 2) return sched == 1 ? (const void*)sim_kernel<2, false> : (const void*)sim_kernel<2, true>;
+    return sched == 1 ? (const void*)sim_kernel<0, false> : (const void*)sim_kernel<0, true>;
+}
 
-int max_coresident_blocks(int device, int engine, int* per_sm) {
+size_t warp_scratch_entries(int blocks) {
+    return (size_t)blocks * (kThreads / 32) * (wv::OBG > (int)sl::kScratchPerWarp ? (size_t)wv::OBG : sl::kScratchPerWarp);
+}
+
+int max_coresident_blocks(int device, int engine, int sched, int* per_sm) {
     int nb = 0, sms = 0;
-    cudaFuncSetAttribute(sim_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wv::kSmemBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sim_kernel, kThreads, dyn_smem(engine));
+    const void* k = kernel_for(engine, sched);
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem(engine));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kThreads, dyn_smem(engine));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm) *per_sm = nb;
     return nb * sms;
@@ -720,7 +947,8 @@ cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s) {
     SimParams q = p;
     q.nblocks = (uint32_t)blocks;
     void* args[] = {&q};
-    return cudaLaunchCooperativeKernel((void*)sim_kernel, dim3(blocks), dim3(kThreads), args, dyn_smem(p.engine), s);
+    return cudaLaunchCooperativeKernel(kernel_for(p.engine, p.sched), dim3(blocks), dim3(kThreads), args,
+                                       dyn_smem(p.engine), s);
 }
 
 cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaStream_t s) {

@@ -3,63 +3,62 @@
 // fallback for pathological chunks).
 //
 // One warp owns one chunk.  Per tile:
-//   1. coalesced refills of a 128-entry shared-memory window per fan-in pin
-//      (Alg. 2 reads each input waveform);
-//   2. the tile = every window entry with t <= T_lim (T_lim = the earliest
-//      last-loaded time of a pin that has more data, so no later entry can
-//      interleave); entries become 32-bit keys (t - base) << 4 | pin << 2 | v;
-//   3. k-way merge by merge path (pairwise for k = 3, 4); lane l receives the
-//      merged entries [l*E, (l+1)*E) in a conflict-free [j][lane] layout;
-//   4. each lane sweeps its entries: input vector (warp scan of composed
-//      updates), distinct timestamps, LUT evaluation, events and delays;
+//   1. coalesced refills of one shared-memory ring per fan-in pin (the k rings
+//      share 512 entries), Alg. 2 reading its input waveforms;
+//   2. the tile = every ring entry with t <= T_lim (T_lim = the earliest
+//      last-loaded time among pins with more data, so no later entry can
+//      interleave), found by binary search per ring;
+//   3. k-way merge by merge path straight from the rings (pairwise for k = 3,
+//      4); lane l receives merged entries [l*E, (l+1)*E) as 32-bit keys
+//      (t - base) << 4 | pin << 2 | v in a conflict-free [j][lane] layout and,
+//      in the same loop, composes its input updates and marks distinct
+//      timestamps;
+//   4. a warp scan of the composed updates gives each lane its input vector;
+//      each lane evaluates the LUT at its distinct timestamps and finds events
+//      and their delays (only the changed pins are visited);
 //   5. Eq. 1 survivors = events whose appearance time is below every later
 //      event's (per-lane reverse minimum + warp suffix minimum); dedupe against
 //      the previous survivor; survivors with r <= T_lim + dmin are final
-//       and go to the per-warp output buffer, later ones stay
+//       and go to the warp's output scratch, later ones stay
 //      pending across tiles.
 // At the end the chunk's exact count is known: one atomic allocates its segment
-// and the buffer is copied out with coalesced stores.  Results are bit-identical
-// to the per-lane engine and the oracle (tests/test_gpu_parity.py).
+// and the scratch is copied out with coalesced stores.  Results are
+// bit-identical to the per-lane engine and the oracle (tests/test_gpu_parity.py).
 #pragma once
 
 namespace gls {
 namespace wv {
 
-constexpr int WIN = 128;                   // window entries per pin (ring, power of 2)
-constexpr int TMAX = 4 * WIN;              // entries per tile at most
+constexpr int RING = 512;                  // ring entries shared by the k pins
+constexpr int TMAX = 512;                  // entries per tile at most
 constexpr int EPL = TMAX / 32;             // entries per lane at most (16)
 constexpr int PMAX = 64;                   // pending schedules carried between tiles
-constexpr int OB = 1024;                   // output buffer entries per warp (>= PMAX + TMAX)
-constexpr int NSPILL = 32;                 // spilled output blocks per chunk
+constexpr int NSPILL = 32;                 // spilled scratch blocks per chunk
 constexpr unsigned FULL = 0xffffffffu;
 constexpr long long SPAN = (1ll << 28) - 1; // key time span of one tile
 constexpr uint32_t RINF = 0xffffffffu;
 
 struct WS {
-    uint64_t win[4][WIN];                  // 4 KB  raw entries, ring per pin
+    uint64_t ring[RING];                   // 4 KB  raw entries; pin i at [i*cap, (i+1)*cap)
     union {
-        struct {                           // live during key build + merge
-            uint32_t key[4][WIN];
-            uint32_t tmpA[2 * WIN];
-            uint32_t tmpB[2 * WIN];
+        struct {                           // level-1 merge outputs (k = 3, 4)
+            uint32_t tmpA[TMAX / 2];
+            uint32_t tmpB[TMAX / 2];
         } m;
-        struct {                           // live during the sweeps ([j][lane] layout)
-            uint32_t evr[EPL][32];         // event appearance time (relative), RINF if none
-            uint8_t gev[EPL][32];          // bit0..1 E value, bit2 group end
-        } s;
-    } u;                                   // 4 KB
-    uint32_t merged[EPL][32];              // 2 KB  merged keys, [j][lane]
+        uint32_t evr[EPL][32];             // event appearance time (relative), RINF if none
+    } u;                                   // 2 KB
+    uint32_t merged[EPL][32];              // 2 KB  merged keys
+    uint8_t gev[EPL][32];                  // 512 B bits 0..1 evaluation
     uint64_t pend[PMAX];                   // 512 B
-    uint64_t out[OB];                      // 8 KB
     unsigned long long spill_off[NSPILL];
     uint32_t spill_cnt[NSPILL];
-    uint32_t dtab[4][2][3];                // per pin: [fall, rise][out 0, 1, X] (R1)
-    // cursors (warp-uniform, written by lane 0)
-    unsigned long long c_off[4];
+    uint32_t dtab[4 * 6];                  // per pin: [fall, rise][out 0, 1, X] (R1)
+    unsigned long long c_off[4];           // cursors (warp-uniform, written by lane 0)
     uint32_t c_rem[4], c_ck[4], c_ckend[4], whead[4], wcnt[4], more[4];
 };
 constexpr int kWarpsPerBlock = kThreads / 32;
 constexpr size_t kSmemBytes = sizeof(WS) * kWarpsPerBlock;
+constexpr int OBG = 4096;                  // per-warp output scratch entries (global memory)
 
 __device__ __forceinline__ uint32_t expand4(uint32_t m) {  // pin bit i -> value field bits 2i, 2i+1
     return ((m & 1u) * 3u) | ((m & 2u) * 6u) | ((m & 4u) * 12u) | ((m & 8u) * 24u);
@@ -71,12 +70,62 @@ __device__ __forceinline__ uint32_t set_pin(uint32_t v, uint32_t key) {
     const uint32_t pin = (key >> 2) & 3u;
     return (v & ~(3u << (2 * pin))) | (norm_code(key & 3u) << (2 * pin));
 }
+__device__ __forceinline__ uint32_t mkkey(uint64_t e, long long tbase, uint32_t pin) {
+    return ((uint32_t)(etime(e) - tbase) << 4) | (pin << 2) | (uint32_t)(e & 3u);
+}
 
-// merge two strictly increasing key lists (keys are unique) with merge path.
-// Output d goes to C[d] (linear) or, if T, to CT[d - d0][lane] (lane's slice).
-template <bool T>
-__device__ __forceinline__ void merge2(const uint32_t* A, int na, const uint32_t* B, int nb, uint32_t* C,
-                                       uint32_t (*CT)[32], int per, int lane) {
+// per-lane accumulation while the final merge emits the lane's entries
+struct LaneAcc {
+    uint32_t upd;      // composed update of the lane's entries (mask << 8 | vals)
+    uint32_t upd_ge;   // composed update up to the lane's last distinct-timestamp end
+    uint32_t gemask;   // bit j: entry j ends a distinct timestamp
+    uint32_t last_t;
+};
+__device__ __forceinline__ void acc_emit(WS& ws, LaneAcc& a, uint32_t key, int j, int lane) {
+    const uint32_t t = key >> 4;
+    if (j > 0 && t != a.last_t) {
+        a.gemask |= 1u << (j - 1);
+        a.upd_ge = a.upd;
+    }
+    const uint32_t pin = (key >> 2) & 3u;
+    a.upd = ((a.upd | (0x100u << pin)) & ~(3u << (2 * pin))) | (norm_code(key & 3u) << (2 * pin));
+    a.last_t = t;
+    ws.merged[j][lane] = key;
+}
+
+// Merge path over two pins' ring prefixes (raw entries; on equal times the
+// lower pin, A, comes first).  FINAL: outputs go to merged[j][lane] with the
+// lane accumulation; else keys go to C[d].
+template <bool FINAL>
+__device__ __forceinline__ void merge_rings(WS& ws, const uint64_t* Ab, uint32_t Ah, uint32_t Am, uint32_t Ap, int na,
+                                            const uint64_t* Bb, uint32_t Bh, uint32_t Bm, uint32_t Bp, int nb,
+                                            long long tbase, uint32_t* C, int per, int lane, LaneAcc& acc) {
+    const int n = na + nb;
+    const int d0 = min(lane * per, n), d1 = min(d0 + per, n);
+    int lo = max(0, d0 - nb), hi = min(d0, na);
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (etime(Ab[(Ah + mid) & Am]) <= etime(Bb[(Bh + d0 - 1 - mid) & Bm])) lo = mid + 1; else hi = mid;
+    }
+    int ia = lo, ib = d0 - lo;
+    uint64_t ha = ia < na ? Ab[(Ah + ia) & Am] : kInfEntry;
+    uint64_t hb = ib < nb ? Bb[(Bh + ib) & Bm] : kInfEntry;
+    for (int d = d0; d < d1; ++d) {
+        const bool takeA = etime(ha) <= etime(hb);
+        const uint32_t key = takeA ? mkkey(ha, tbase, Ap) : mkkey(hb, tbase, Bp);
+        if (takeA) {
+            ++ia;
+            ha = ia < na ? Ab[(Ah + ia) & Am] : kInfEntry;
+        } else {
+            ++ib;
+            hb = ib < nb ? Bb[(Bh + ib) & Bm] : kInfEntry;
+        }
+        if (FINAL) acc_emit(ws, acc, key, d - d0, lane); else C[d] = key;
+    }
+}
+// merge path over two key arrays (keys unique, pins distinct across A and B)
+__device__ __forceinline__ void merge_keys(WS& ws, const uint32_t* A, int na, const uint32_t* B, int nb, int per,
+                                           int lane, LaneAcc& acc) {
     const int n = na + nb;
     const int d0 = min(lane * per, n), d1 = min(d0 + per, n);
     int lo = max(0, d0 - nb), hi = min(d0, na);
@@ -85,12 +134,12 @@ __device__ __forceinline__ void merge2(const uint32_t* A, int na, const uint32_t
         if (A[mid] < B[d0 - 1 - mid]) lo = mid + 1; else hi = mid;
     }
     int ia = lo, ib = d0 - lo;
+    uint32_t ha = ia < na ? A[ia] : RINF, hb = ib < nb ? B[ib] : RINF;
     for (int d = d0; d < d1; ++d) {
-        const bool takeA = ib >= nb || (ia < na && A[ia] < B[ib]);
-        const uint32_t v = takeA ? A[ia] : B[ib];
-        ia += takeA;
-        ib += !takeA;
-        if (T) CT[d - d0][lane] = v; else C[d] = v;
+        const bool takeA = ha < hb;
+        const uint32_t key = takeA ? ha : hb;
+        if (takeA) { ++ia; ha = ia < na ? A[ia] : RINF; } else { ++ib; hb = ib < nb ? B[ib] : RINF; }
+        acc_emit(ws, acc, key, d - d0, lane);
     }
 }
 
@@ -101,21 +150,15 @@ struct Emit {   // per-chunk output state (warp-uniform)
     uint32_t last_val;
 };
 
-// spill the output buffer to the deep-scratch pool; false if out of room
-__device__ __noinline__ bool spill(const SimParams& p, WS& ws, Emit& em, int lane) {
+// move the warp's output scratch to the deep-scratch pool; false if out of room
+__device__ __noinline__ bool spill(const SimParams& p, WS& ws, uint64_t* scr, Emit& em, int lane) {
     if (em.out_n == 0) return true;
     if (em.nspill >= NSPILL) return false;
     unsigned long long at = 0;
-    if (lane == 0) at = atomicAdd(&p.ctl->deep_top, (unsigned long long)em.out_n);
+    if (lane == 0) at = deep_alloc(p, (unsigned long long)em.out_n);
     at = __shfl_sync(FULL, at, 0);
-    if (at + (unsigned long long)em.out_n > p.deep_cap) {
-        if (lane == 0) {
-            atomicOr(&p.ctl->error, kErrDeep);
-            atomicMax(&p.ctl->need_deep, at + (unsigned long long)em.out_n);
-        }
-        return false;
-    }
-    for (int q = lane; q < em.out_n; q += 32) p.deep[at + q] = ws.out[q];
+    if (at == ~0ull) return false;
+    for (int q = lane; q < em.out_n; q += 32) p.deep[at + q] = scr[q];
     if (lane == 0) {
         ws.spill_off[em.nspill] = at;
         ws.spill_cnt[em.nspill] = (uint32_t)em.out_n;
@@ -126,14 +169,15 @@ __device__ __noinline__ bool spill(const SimParams& p, WS& ws, Emit& em, int lan
     return true;
 }
 
-// coalesced refill of pin i's window up to WIN entries (warp-uniform control)
-__device__ __forceinline__ void refill(const SimParams& p, WS& ws, int i, long long T1, int lane) {
+// coalesced refill of pin i's ring up to `cap` entries (warp-uniform control)
+__device__ __forceinline__ void refill(const SimParams& p, WS& ws, int i, uint32_t cap, long long T1, int lane) {
     uint32_t wc = ws.wcnt[i], more = ws.more[i];
-    if (!more || wc >= (uint32_t)WIN) return;
+    if (!more || wc >= cap) return;
     unsigned long long off = ws.c_off[i];
     uint32_t rem = ws.c_rem[i], ck = ws.c_ck[i];
-    const uint32_t ckend = ws.c_ckend[i], wh = ws.whead[i];
-    while (more && wc < (uint32_t)WIN) {
+    const uint32_t ckend = ws.c_ckend[i], wh = ws.whead[i], m = cap - 1;
+    uint64_t* rb = ws.ring + i * cap;
+    while (more && wc < cap) {
         if (rem == 0) {
             if (ck + 1 < ckend) {
                 ++ck;
@@ -144,17 +188,14 @@ __device__ __forceinline__ void refill(const SimParams& p, WS& ws, int i, long l
             more = 0;
             break;
         }
-        const uint32_t take = min(min((uint32_t)WIN - wc, rem), 32u);
-        uint64_t e = 0;
-        if ((uint32_t)lane < take) {
-            e = p.arena[off + lane];
-            ws.win[i][(wh + wc + lane) & (WIN - 1)] = e;
-        }
-        const uint64_t last = __shfl_sync(FULL, e, take - 1);
+        const uint32_t take = min(cap - wc, rem);
+#pragma unroll 4
+        for (uint32_t q = lane; q < take; q += 32) rb[(wh + wc + q) & m] = p.arena[off + q];
         off += take;
         rem -= take;
         wc += take;
-        if (etime(last) >= T1) more = 0;   // later entries cannot matter
+        __syncwarp();
+        if (etime(rb[(wh + wc - 1) & m]) >= T1) more = 0;   // later entries cannot matter
     }
     __syncwarp();
     if (lane == 0) {
@@ -180,23 +221,26 @@ __device__ __forceinline__ uint32_t excl_last_valid(uint32_t y, int lane) {
 
 // Returns false when the chunk must be redone by the per-lane engine
 // (pending list or spill list overflow).
-__device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkSetup& s, const uint8_t* lut,
-                                        unsigned long long& out_off, uint32_t& out_cnt, uint32_t& out_vb,
-                                        unsigned long long& evals, unsigned long long& events, bool& fits) {
+__device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, uint64_t* scr, const ChunkSetup& s,
+                                        const uint8_t* lut, unsigned long long& out_off, uint32_t& out_cnt,
+                                        uint32_t& out_vb, unsigned long long& evals, unsigned long long& events,
+                                        bool& fits) {
     const int lane = threadIdx.x & 31;
     const int k = (int)s.k;
+    const uint32_t cap = k == 1 ? RING : (k == 2 ? RING / 2 : RING / 4);
     const uint32_t lb = s.lut_base;
     const long long T0 = s.T0, T1 = s.T1, dur = p.duration, dmin = (long long)s.dmin;
 
     // delay tables (reading R1: output X takes the smaller of the two)
     if (lane < 4) {
         const uint4 d = lane == 0 ? s.d[0] : lane == 1 ? s.d[1] : lane == 2 ? s.d[2] : s.d[3];
-        ws.dtab[lane][1][0] = d.x;                 // RISE -> 0
-        ws.dtab[lane][1][1] = d.y;                 // RISE -> 1
-        ws.dtab[lane][1][2] = min(d.x, d.y);
-        ws.dtab[lane][0][0] = d.z;                 // FALL -> 0
-        ws.dtab[lane][0][1] = d.w;                 // FALL -> 1
-        ws.dtab[lane][0][2] = min(d.z, d.w);
+        uint32_t* t = ws.dtab + lane * 6;
+        t[3] = d.x;               // RISE -> 0
+        t[4] = d.y;               // RISE -> 1
+        t[5] = min(d.x, d.y);
+        t[0] = d.z;               // FALL -> 0
+        t[1] = d.w;               // FALL -> 1
+        t[2] = min(d.z, d.w);
     }
     // cursors: lane i locates pin i at tau0 (first transition > tau0, value at tau0)
     uint32_t l_init = 2;
@@ -226,7 +270,7 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
             uint32_t del = RINF;
             for (int i = 0; i < k; ++i) {
                 const uint32_t f = (x0 >> (2 * i)) & 3u;
-                if (f != 2u) del = min(del, ws.dtab[i][f == 1u ? 1 : 0][E0]);
+                if (f != 2u) del = min(del, ws.dtab[i * 6 + (f == 1u ? 3 : 0) + E0]);
             }
             if (lane == 0) ws.pend[0] = ((uint64_t)(s.tau0 + (long long)del) << 2) | E0;
             np = 1;
@@ -236,75 +280,74 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
     unsigned long long n_evals = 0, n_events = 0;
 
     for (;;) {
-        // ---- 1. refill windows (coalesced)
-        for (int i = 0; i < k; ++i) refill(p, ws, i, T1, lane);
+        // ---- 1. refill rings (coalesced)
+        for (int i = 0; i < k; ++i) refill(p, ws, i, cap, T1, lane);
         // ---- 2. tile bounds
         long long tbase = LLONG_MAX, tsafe = LLONG_MAX;
         for (int i = 0; i < k; ++i) {
             const uint32_t wc = ws.wcnt[i], wh = ws.whead[i];
+            const uint64_t* rb = ws.ring + i * cap;
             if (wc > 0) {
-                tbase = min(tbase, etime(ws.win[i][wh]));
-                if (ws.more[i]) tsafe = min(tsafe, etime(ws.win[i][(wh + wc - 1) & (WIN - 1)]));
+                tbase = min(tbase, etime(rb[wh]));
+                if (ws.more[i]) tsafe = min(tsafe, etime(rb[(wh + wc - 1) & (cap - 1)]));
             }
         }
         if (tbase >= T1) break;                               // nothing left before T1
         const long long tlim = min(min(tsafe, T1 - 1), tbase + SPAN);
         int mi[4] = {0, 0, 0, 0};
         int nt = 0;
-        for (int i = 0; i < k; ++i) {
-            const uint32_t wc = ws.wcnt[i], wh = ws.whead[i];
-            int m = 0;
-#pragma unroll
-            for (int q = 0; q < WIN / 32; ++q) {
-                const uint32_t j = lane + 32 * q;
-                const uint64_t e = j < wc ? ws.win[i][(wh + j) & (WIN - 1)] : kInfEntry;
-                const bool pr = j < wc && etime(e) <= tlim;
-                m += __popc(__ballot_sync(FULL, pr));
-                if (pr) ws.u.m.key[i][j] = ((uint32_t)(etime(e) - tbase) << 4) | ((uint32_t)i << 2) | (uint32_t)(e & 3u);
+        for (int i = 0; i < k; ++i) {                         // entries with t <= tlim
+            const uint64_t* rb = ws.ring + i * cap;
+            const uint32_t wh = ws.whead[i];
+            int lo = 0, hi = (int)ws.wcnt[i];
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (etime(rb[(wh + mid) & (cap - 1)]) <= tlim) lo = mid + 1; else hi = mid;
             }
-            mi[i] = m;
-            nt += m;
+            mi[i] = lo;
+            nt += lo;
         }
-        __syncwarp();
-        // ---- 3. k-way merge; lane l gets merged entries [l*Ep, l*Ep + nv) in merged[j][l]
+        // ---- 3. merge; lane l gets merged entries [l*Ep, l*Ep + nv)
         const int Ep = (nt + 31) >> 5;
         const int nv = max(0, min(Ep, nt - lane * Ep));
+        LaneAcc acc{0u, 0u, 0u, 0u};
         if (k == 1) {
-            for (int j = 0; j < nv; ++j) ws.merged[j][lane] = ws.u.m.key[0][lane * Ep + j];
+            const uint64_t* rb = ws.ring;
+            const uint32_t wh = ws.whead[0];
+            for (int j = 0; j < nv; ++j)
+                acc_emit(ws, acc, mkkey(rb[(wh + lane * Ep + j) & (cap - 1)], tbase, 0u), j, lane);
         } else if (k == 2) {
-            merge2<true>(ws.u.m.key[0], mi[0], ws.u.m.key[1], mi[1], nullptr, ws.merged, Ep, lane);
-        } else if (k == 3) {
-            const int n01 = mi[0] + mi[1];
-            merge2<false>(ws.u.m.key[0], mi[0], ws.u.m.key[1], mi[1], ws.u.m.tmpA, nullptr, (n01 + 31) >> 5, lane);
-            __syncwarp();
-            merge2<true>(ws.u.m.tmpA, n01, ws.u.m.key[2], mi[2], nullptr, ws.merged, Ep, lane);
+            merge_rings<true>(ws, ws.ring, ws.whead[0], cap - 1, 0u, mi[0], ws.ring + cap, ws.whead[1], cap - 1, 1u,
+                              mi[1], tbase, nullptr, Ep, lane, acc);
         } else {
-            const int n01 = mi[0] + mi[1], n23 = mi[2] + mi[3];
-            merge2<false>(ws.u.m.key[0], mi[0], ws.u.m.key[1], mi[1], ws.u.m.tmpA, nullptr, (n01 + 31) >> 5, lane);
-            merge2<false>(ws.u.m.key[2], mi[2], ws.u.m.key[3], mi[3], ws.u.m.tmpB, nullptr, (n23 + 31) >> 5, lane);
+            const int n01 = mi[0] + mi[1];
+            merge_rings<false>(ws, ws.ring, ws.whead[0], cap - 1, 0u, mi[0], ws.ring + cap, ws.whead[1], cap - 1, 1u,
+                               mi[1], tbase, ws.u.m.tmpA, (n01 + 31) >> 5, lane, acc);
+            int n23;
+            if (k == 3) {
+                n23 = mi[2];
+                const uint64_t* rb = ws.ring + 2 * cap;
+                const uint32_t wh = ws.whead[2];
+                for (int q = lane; q < n23; q += 32) ws.u.m.tmpB[q] = mkkey(rb[(wh + q) & (cap - 1)], tbase, 2u);
+            } else {
+                n23 = mi[2] + mi[3];
+                merge_rings<false>(ws, ws.ring + 2 * cap, ws.whead[2], cap - 1, 2u, mi[2], ws.ring + 3 * cap,
+                                   ws.whead[3], cap - 1, 3u, mi[3], tbase, ws.u.m.tmpB, (n23 + 31) >> 5, lane, acc);
+            }
             __syncwarp();
-            merge2<true>(ws.u.m.tmpA, n01, ws.u.m.tmpB, n23, nullptr, ws.merged, Ep, lane);
+            merge_keys(ws, ws.u.m.tmpA, n01, ws.u.m.tmpB, n23, Ep, lane, acc);
         }
         __syncwarp();
-        // the entry after my last one (next lane's first), for timestamp grouping
-        const uint32_t nxt = (lane < 31 && (lane + 1) * Ep < nt) ? ws.merged[0][lane + 1] : RINF;
-        const uint32_t tnxt = nxt == RINF ? RINF : (nxt >> 4);
-
-        // ---- 4a. compose input updates (whole lane and up to the last group end)
-        uint32_t upd = 0, upd_ge = 0;
-        bool has_ge = false;
-        for (int j = 0; j < nv; ++j) {
-            const uint32_t key = ws.merged[j][lane];
-            const uint32_t pin = (key >> 2) & 3u;
-            upd = (upd | (0x100u << pin));
-            upd = (upd & ~(3u << (2 * pin))) | (norm_code(key & 3u) << (2 * pin));
-            const uint32_t tn = j + 1 < nv ? (ws.merged[j + 1][lane] >> 4) : tnxt;
-            if (tn != (key >> 4)) {
-                upd_ge = upd;
-                has_ge = true;
+        // close the lane's last timestamp group against the next lane's first entry
+        {
+            const uint32_t tn = (lane < 31 && (lane + 1) * Ep < nt) ? (ws.merged[0][lane + 1] >> 4) : RINF;
+            if (nv > 0 && tn != acc.last_t) {
+                acc.gemask |= 1u << (nv - 1);
+                acc.upd_ge = acc.upd;
             }
         }
-        uint32_t x = upd;
+        // ---- 4. input vectors: warp scan of the composed updates
+        uint32_t x = acc.upd;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(FULL, x, o);
@@ -314,13 +357,12 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
         const uint32_t xe = lane == 0 ? 0u : xe0;
         const uint32_t xtot = __shfl_sync(FULL, x, 31);
         const uint32_t vstart = apply_upd(vec_carry, xe);
-        // vector at the previous timestamp before my first group end
-        const uint32_t tagged = has_ge ? (0x100u | apply_upd(vstart, upd_ge)) : 0u;
+        // vector at the previous distinct timestamp before my first group end
         uint32_t vprev;
         {
+            const uint32_t tagged = acc.gemask ? (0x100u | apply_upd(vstart, acc.upd_ge)) : 0u;
             const unsigned lanes_with = __ballot_sync(FULL, nv > 0);
-            const unsigned lanes_ge = __ballot_sync(FULL, has_ge);
-            // every lane before the last populated one holds a group end -> one shuffle
+            const unsigned lanes_ge = __ballot_sync(FULL, acc.gemask != 0u);
             const unsigned need = lanes_with & ~(1u << (31 - __clz(lanes_with | 1u)));
             uint32_t t;
             if ((need & ~lanes_ge) == 0u) {
@@ -331,30 +373,26 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
             }
             vprev = (t & 0x100u) ? (t & 0xffu) : vec_carry;
         }
-        // ---- 4b. evaluations and events (Alg. 2; delays P:210)
+        // ---- 5. evaluations and events (Alg. 2; delays P:210)
         const uint32_t thr = T0 <= tbase ? 0u : (uint32_t)min(T0 - tbase, (long long)(1 << 28));
         uint32_t Eprev = lut[lb + vprev];
-        uint32_t v = vstart;
-        uint32_t lmin = RINF;
-        uint32_t cnt_ge = 0, cnt_ev = 0;
+        uint32_t v = vstart, lmin = RINF, cnt_ge = 0, cnt_ev = 0;
         for (int j = 0; j < nv; ++j) {
             const uint32_t key = ws.merged[j][lane];
             v = set_pin(v, key);
-            const uint32_t tj = key >> 4;
-            const uint32_t tn = j + 1 < nv ? (ws.merged[j + 1][lane] >> 4) : tnxt;
             uint32_t r = RINF, g = 0;
-            if (tn != tj) {
+            if ((acc.gemask >> j) & 1u) {
+                const uint32_t tj = key >> 4;
                 const uint32_t E = lut[lb + v];
                 cnt_ge += tj >= thr;
-                g = 4u | E;
+                g = E;
                 if (E != Eprev) {
                     uint32_t del = RINF;
-                    const uint32_t diff = v ^ vprev;
-                    for (int i = 0; i < k; ++i) {
-                        if ((diff >> (2 * i)) & 3u) {
-                            const uint32_t fo = (vprev >> (2 * i)) & 3u, fn = (v >> (2 * i)) & 3u;
-                            del = min(del, ws.dtab[i][rank_code(fn) > rank_code(fo) ? 1 : 0][E]);
-                        }
+                    const uint32_t d = v ^ vprev;
+                    for (uint32_t cm = (d | (d >> 1)) & 0x55u; cm; cm &= cm - 1) {
+                        const int b = __ffs(cm) - 1;        // 2 * pin
+                        const uint32_t fo = (vprev >> b) & 3u, fn = (v >> b) & 3u;
+                        del = min(del, ws.dtab[(b >> 1) * 6 + (rank_code(fn) > rank_code(fo) ? 3 : 0) + E]);
                     }
                     r = tj + del;
                     lmin = min(lmin, r);
@@ -363,12 +401,12 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
                 vprev = v;
                 Eprev = E;
             }
-            ws.u.s.evr[j][lane] = r;
-            ws.u.s.gev[j][lane] = (uint8_t)g;
+            ws.u.evr[j][lane] = r;
+            ws.gev[j][lane] = (uint8_t)g;
         }
         n_evals += cnt_ge;
         n_events += cnt_ev;
-        // ---- 5. Eq. 1 survivors: r below every later event's r
+        // ---- 6. Eq. 1 survivors: r below every later event's r
         uint32_t sm = lmin;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -380,9 +418,9 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
         const uint32_t tile_min = __shfl_sync(FULL, sm, 0);
         uint32_t survmask = 0, lsv = 0;
         for (int j = nv - 1; j >= 0; --j) {
-            const uint32_t r = ws.u.s.evr[j][lane];
-            if (r < run) {                                   // r == RINF never passes
-                if (!survmask) lsv = ws.u.s.gev[j][lane] & 3u;
+            const uint32_t r = ws.u.evr[j][lane];
+            if (r < run) {                                   // RINF never passes
+                if (!survmask) lsv = ws.gev[j][lane] & 3u;
                 survmask |= 1u << j;
                 run = r;
             }
@@ -408,7 +446,7 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
         if (n_surv > 0) pred_init = (uint32_t)(ws.pend[n_surv - 1] & 3u);
         if (bva | bvb) em.vb = (uint32_t)(ws.pend[bvb ? 32 + 31 - __clz(bvb) : 31 - __clz(bva)] & 3u);
         if (n_fin > 0) em.last_val = (uint32_t)(ws.pend[n_fin - 1] & 3u);
-        // dedupe predecessor of my first survivor
+        // ---- 7. dedupe, final / pending, outputs
         uint32_t prevv;
         {
             const uint32_t t = excl_last_valid(survmask ? (0x100u | lsv) : 0u, lane);
@@ -416,15 +454,14 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
         }
         const uint64_t lim_rel64 = (uint64_t)(tlim - tbase) + (uint64_t)dmin;
         const uint32_t lim_rel = lim_rel64 >= RINF ? RINF - 1 : (uint32_t)lim_rel64;
-        uint32_t finmask = 0, pendmask = 0, outmask = 0;
+        uint32_t pendmask = 0, outmask = 0;
         int last_fin_j = -1, last_vb_j = -1;
         for (uint32_t m = survmask; m; m &= m - 1) {
             const int j = __ffs(m) - 1;
-            const uint32_t E = ws.u.s.gev[j][lane] & 3u;
+            const uint32_t E = ws.gev[j][lane] & 3u;
             if (E != prevv) {
-                const uint32_t r = ws.u.s.evr[j][lane];
+                const uint32_t r = ws.u.evr[j][lane];
                 if (r <= lim_rel) {
-                    finmask |= 1u << j;
                     last_fin_j = j;
                     const long long ra = tbase + (long long)r;
                     if (ra < T0) last_vb_j = j;
@@ -447,27 +484,27 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
         const int tot_out = (int)(pre_tot & 0xffffu), tot_pend = (int)(pre_tot >> 16);
         const int keep_old = n_surv - n_fin;
         if (keep_old + tot_pend > PMAX) return false;           // pending overflow -> per-lane engine
-        if (em.out_n + n_oout + tot_out > OB) {
-            if (!spill(p, ws, em, lane)) return false;
+        if (em.out_n + n_oout + tot_out > OBG) {
+            if (!spill(p, ws, scr, em, lane)) return false;
         }
         // outputs: old finals, then tile finals, in order
-        if (oa) ws.out[em.out_n + __popc(boa & ((1u << lane) - 1u))] = pa;
-        if (ob) ws.out[em.out_n + __popc(boa) + __popc(bob & ((1u << lane) - 1u))] = pb;
+        if (oa) scr[em.out_n + __popc(boa & ((1u << lane) - 1u))] = pa;
+        if (ob) scr[em.out_n + __popc(boa) + __popc(bob & ((1u << lane) - 1u))] = pb;
         {
             int q = em.out_n + n_oout + (int)(pre & 0xffffu);
             for (uint32_t m = outmask; m; m &= m - 1) {
                 const int j = __ffs(m) - 1;
-                const long long ra = tbase + (long long)ws.u.s.evr[j][lane];
-                ws.out[q++] = ((uint64_t)ra << 2) | (ws.u.s.gev[j][lane] & 3u);
+                const long long ra = tbase + (long long)ws.u.evr[j][lane];
+                scr[q++] = ((uint64_t)ra << 2) | (ws.gev[j][lane] & 3u);
             }
         }
         {   // value before T0 and last final value from the tile
             const unsigned bl = __ballot_sync(FULL, last_vb_j >= 0);
-            const uint32_t vvb = last_vb_j >= 0 ? ws.u.s.gev[last_vb_j][lane] & 3u : 0u;
+            const uint32_t vvb = last_vb_j >= 0 ? ws.gev[last_vb_j][lane] & 3u : 0u;
             const uint32_t wvb = __shfl_sync(FULL, vvb, bl ? 31 - __clz(bl) : 0);
             if (bl) em.vb = wvb;
             const unsigned bf = __ballot_sync(FULL, last_fin_j >= 0);
-            const uint32_t vlf = last_fin_j >= 0 ? ws.u.s.gev[last_fin_j][lane] & 3u : 0u;
+            const uint32_t vlf = last_fin_j >= 0 ? ws.gev[last_fin_j][lane] & 3u : 0u;
             const uint32_t wlf = __shfl_sync(FULL, vlf, bf ? 31 - __clz(bf) : 0);
             if (bf) em.last_val = wlf;
         }
@@ -479,7 +516,7 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
             int q = keep_old + (int)(pre >> 16);
             for (uint32_t m = pendmask; m; m &= m - 1) {
                 const int j = __ffs(m) - 1;
-                ws.pend[q++] = ((uint64_t)(tbase + (long long)ws.u.s.evr[j][lane]) << 2) | (ws.u.s.gev[j][lane] & 3u);
+                ws.pend[q++] = ((uint64_t)(tbase + (long long)ws.u.evr[j][lane]) << 2) | (ws.gev[j][lane] & 3u);
             }
         }
         np = keep_old + tot_pend;
@@ -487,7 +524,7 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
         // consume the tile
         if (lane < k) {
             const int m = lane == 0 ? mi[0] : lane == 1 ? mi[1] : lane == 2 ? mi[2] : mi[3];
-            ws.whead[lane] = (ws.whead[lane] + (uint32_t)m) & (WIN - 1);
+            ws.whead[lane] = (ws.whead[lane] + (uint32_t)m) & (cap - 1);
             ws.wcnt[lane] -= (uint32_t)m;
         }
         __syncwarp();
@@ -502,11 +539,11 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
         const bool ob = lane + 32 < np && etime(pb) >= T0 && etime(pb) < T1 && etime(pb) <= dur;
         const uint32_t boa = __ballot_sync(FULL, oa), bob = __ballot_sync(FULL, ob);
         const int n = __popc(boa) + __popc(bob);
-        if (em.out_n + n > OB) {
-            if (!spill(p, ws, em, lane)) return false;
+        if (em.out_n + n > OBG) {
+            if (!spill(p, ws, scr, em, lane)) return false;
         }
-        if (oa) ws.out[em.out_n + __popc(boa & ((1u << lane) - 1u))] = pa;
-        if (ob) ws.out[em.out_n + __popc(boa) + __popc(bob & ((1u << lane) - 1u))] = pb;
+        if (oa) scr[em.out_n + __popc(boa & ((1u << lane) - 1u))] = pa;
+        if (ob) scr[em.out_n + __popc(boa) + __popc(bob & ((1u << lane) - 1u))] = pb;
         const uint32_t bva = __ballot_sync(FULL, lane < np && etime(pa) < T0);
         const uint32_t bvb = __ballot_sync(FULL, lane + 32 < np && etime(pb) < T0);
         if (bva | bvb) em.vb = (uint32_t)(ws.pend[bvb ? 32 + 31 - __clz(bvb) : 31 - __clz(bva)] & 3u);
@@ -516,16 +553,9 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
     // exact allocation of the chunk's segment and coalesced copy-out
     uint32_t total = (uint32_t)em.out_n;
     for (int q = 0; q < em.nspill; ++q) total += ws.spill_cnt[q];
-    unsigned long long at = 0;
-    if (lane == 0 && total) at = atomicAdd(&p.ctl->arena_top, (unsigned long long)total);
-    at = __shfl_sync(FULL, at, 0);
-    fits = at + total <= p.arena_cap;
-    if (!fits) {
-        if (lane == 0) {
-            atomicOr(&p.ctl->error, kErrArena);
-            atomicMax(&p.ctl->need_arena, at + total);
-        }
-    } else {
+    const unsigned long long at = arena_alloc(p, total);
+    fits = at != ~0ull;
+    if (fits) {
         unsigned long long o = at;
         for (int q = 0; q < em.nspill; ++q) {
             const unsigned long long so = ws.spill_off[q];
@@ -533,7 +563,7 @@ __device__ __noinline__ bool warp_chunk(const SimParams& p, WS& ws, const ChunkS
             for (uint32_t e = lane; e < sc; e += 32) p.arena[o + e] = p.deep[so + e];
             o += sc;
         }
-        for (int e = lane; e < em.out_n; e += 32) p.arena[o + e] = ws.out[e];
+        for (int e = lane; e < em.out_n; e += 32) p.arena[o + e] = scr[e];
     }
     __syncwarp();
     out_off = at;

@@ -36,7 +36,8 @@ class GlsError(RuntimeError):
 class gls_config(ctypes.Structure):
     _fields_ = [("arena_bytes", ctypes.c_int64), ("chunk_capacity", ctypes.c_int64),
                 ("chunk_events", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
-                ("ring_limit", ctypes.c_int32), ("engine", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+                ("ring_limit", ctypes.c_int32), ("engine", ctypes.c_int32), ("scheduler", ctypes.c_int32),
+                ("deep_per_warp", ctypes.c_int64), ("reserved", ctypes.c_int32 * 2)]
 
 
 class gls_stats(ctypes.Structure):
@@ -154,8 +155,9 @@ class Context:
 
     # ---- ABI calls ----------------------------------------------------------
     def gls_set_config(self, arena_bytes=0, chunk_capacity=0, chunk_events=0, blocks_per_sm=0, ring_limit=0,
-                       engine=0):
-        c = gls_config(arena_bytes, chunk_capacity, chunk_events, blocks_per_sm, ring_limit, engine)
+                       engine=0, scheduler=0, deep_per_warp=0):
+        c = gls_config(arena_bytes, chunk_capacity, chunk_events, blocks_per_sm, ring_limit, engine, scheduler,
+                       deep_per_warp)
         return self._check(self._lib.gls_set_config(self._h, ctypes.byref(c)))
 
     def gls_load_netlist(self, num_inputs, gate_type, fanin_offsets, fanin_net, pin_delay):

@@ -25,7 +25,10 @@ def run_oracle(nl, st, dur):
                            nl.pin_delay, st.offsets, st.trans, dur)
 
 
-ENGINES = [0, 1]   # 0 = warp-cooperative, 1 = per-lane
+# engine 0 = lane slices (default), 1 = per-lane chunks, 2 = warp-cooperative tiles;
+# scheduler 0 = dataflow (default), 1 = level barriers
+ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1), dict(engine=2), dict(engine=2, scheduler=1)]
+EIDS = ["slice-df", "slice-lvl", "lane", "warp-df", "warp-lvl"]
 
 
 def run_gpu(c, nl, st, dur, **cfg):
@@ -52,17 +55,17 @@ def assert_same(c, nl, st, dur, ref=None, hashes=True, **cfg):
     return s
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 @pytest.mark.parametrize("ex", golden_io.examples(), ids=lambda e: e.name)
 def test_worked_examples(ctx, ex, engine):
     nl, st, dur, index, exp = ex.build()
-    w, _ = run_gpu(ctx, nl, st, dur, engine=engine)
+    w, _ = run_gpu(ctx, nl, st, dur, **engine)
     for net, wave in exp.items():
         assert w.wave(net) == wave, (ex.name, nl.names[net])
-    assert_same(ctx, nl, st, dur, engine=engine)
+    assert_same(ctx, nl, st, dur, **engine)
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 def test_random_designs_1000(ctx, engine):
     """SPEC-style acceptance: >= 1000 random designs."""
     rng = np.random.Generator(np.random.PCG64(2024))
@@ -73,12 +76,12 @@ def test_random_designs_1000(ctx, engine):
         st = W.random_stimuli(d, P, int(rng.integers(0, 40)), 400, xz=float(rng.random() * 0.3),
                               max_gap=int(rng.integers(1, 30)))
         try:
-            assert_same(ctx, nl, st, 450, hashes=(d % 10 == 0), engine=engine)
+            assert_same(ctx, nl, st, 450, hashes=(d % 10 == 0), **engine)
         except AssertionError as e:
             raise AssertionError(f"design {d}: {e}")
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 @pytest.mark.parametrize("M", [1, 2, 3, 5, 17, 300])
 def test_small_chunks_exact(ctx, M, engine):
     """Many (gate, time-chunk) items per gate: halo starts, chunk value-before
@@ -86,7 +89,7 @@ def test_small_chunks_exact(ctx, M, engine):
     for seed in range(15):
         nl = W.random_dag(500 + seed, 6, 80, max_delay=20)
         st = W.random_stimuli(seed, 6, 60, 3000, xz=0.1, max_gap=60)
-        assert_same(ctx, nl, st, 3100, chunk_events=M, hashes=False, engine=engine)
+        assert_same(ctx, nl, st, 3100, chunk_events=M, hashes=False, **engine)
 
 
 @pytest.mark.parametrize("ring", [1, 2, 3])
@@ -101,38 +104,38 @@ def test_deep_backtrace_path(ctx, ring):
     assert deep > 0
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 def test_zero_and_huge_delays(ctx, engine):
     for seed in range(10):
         nl = W.random_dag(800 + seed, 4, 50, max_delay=0)
         st = W.random_stimuli(seed, 4, 30, 200, xz=0.3)
-        assert_same(ctx, nl, st, 250, hashes=False, engine=engine)
+        assert_same(ctx, nl, st, 250, hashes=False, **engine)
     nl = W.random_dag(900, 4, 40, max_delay=10)
     nl.pin_delay[::3] = (1 << 31) - 1
     st = W.random_stimuli(9, 4, 30, 200)
-    assert_same(ctx, nl, st, 250, engine=engine)
-    assert_same(ctx, nl, st, (1 << 33), engine=engine)
+    assert_same(ctx, nl, st, 250, **engine)
+    assert_same(ctx, nl, st, (1 << 33), **engine)
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 def test_large_times(ctx, engine):
     base = 1 << 59
     nl = W.random_dag(901, 3, 30, max_delay=50)
     waves = [[(base + 10 * j + p, (j + p) % 2) for j in range(20)] for p in range(3)]
     st = W.stimuli_from_lists(waves)
-    assert_same(ctx, nl, st, (1 << 61) - 1, engine=engine)
+    assert_same(ctx, nl, st, (1 << 61) - 1, **engine)
     # sparse, far-apart transitions: tiles limited by the 2^28 ps key span
     waves = [[(j * (1 << 29) + 7 * p, (j + p) % 2) for j in range(12)] for p in range(3)]
-    assert_same(ctx, nl, W.stimuli_from_lists(waves), 13 * (1 << 29), engine=engine)
+    assert_same(ctx, nl, W.stimuli_from_lists(waves), 13 * (1 << 29), **engine)
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 def test_empty_and_constant_inputs(ctx, engine):
     nl = W.random_dag(902, 4, 30, max_delay=5)
     st = W.stimuli_from_lists([[], [], [], []])
-    assert_same(ctx, nl, st, 100, engine=engine)
+    assert_same(ctx, nl, st, 100, **engine)
     st = W.stimuli_from_lists([[(0, 1)], [], [(5, 3)], [(0, 0), (7, 2)]])
-    assert_same(ctx, nl, st, 100, engine=engine)
+    assert_same(ctx, nl, st, 100, **engine)
     # PIs only
     nl0 = W.netlist_from_gates(2, [])
     st0 = W.stimuli_from_lists([[(1, 0)], [(2, 3), (4, 1)]])
@@ -140,13 +143,13 @@ def test_empty_and_constant_inputs(ctx, engine):
     assert w.wave(1) == [(2, 3), (4, 1)] and s["gate_evals"] == 0
 
 
-@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 def test_c7552_shaped(ctx, engine):
     nl = W.config_netlist("c7552")
     spec = W.config_stimspec("c7552")
     o, t = W.generate_stimuli(spec)
     st = W.Stimuli(o.numpy(), t.numpy().astype(np.uint64))
-    s = assert_same(ctx, nl, st, spec.duration, engine=engine)
+    s = assert_same(ctx, nl, st, spec.duration, **engine)
     assert s["gate_evals"] > 1_000_000
 
 
@@ -158,7 +161,8 @@ def test_determinism_and_launch_shapes(ctx):
     ref = run_oracle(nl, st, spec.duration)
     base = None
     for cfg in [dict(), dict(blocks_per_sm=1), dict(chunk_events=32), dict(chunk_events=4096), dict(engine=1),
-                dict(engine=1, chunk_events=64), dict()]:
+                dict(engine=1, chunk_events=64), dict(engine=2), dict(engine=2, chunk_events=64),
+                dict(scheduler=1), dict(scheduler=1, chunk_events=64), dict(deep_per_warp=64), dict()]:
         w, _ = run_gpu(ctx, nl, st, spec.duration, **cfg)
         assert np.array_equal(w.trans, ref.trans)
         if base is None:
@@ -243,7 +247,11 @@ def test_warp_engine_deep_pending_and_spills(ctx, seed):
     list (-> per-lane fallback); long single-chunk gates spill its output buffer."""
     nl = W.random_dag(1200 + seed, 4, 40, max_delay=400, min_delay=0)
     st = W.random_stimuli(seed, 4, 600, 3000, xz=0.05, min_gap=1, max_gap=3)
-    s = assert_same(ctx, nl, st, 4000, engine=0, chunk_events=1 << 20, hashes=False)
+    for eng in (0, 2):
+        for sch in (0, 1):
+            assert_same(ctx, nl, st, 4000, engine=eng, scheduler=sch, chunk_events=1 << 20, hashes=False)
     nl = W.random_dag(1300 + seed, 3, 30, max_delay=2, types=[W.BUF, W.NOT, W.XOR])
     st = W.random_stimuli(seed, 3, 3000, 60000, xz=0.0, min_gap=5, max_gap=30)
-    assert_same(ctx, nl, st, 61000, engine=0, chunk_events=1 << 20, hashes=False)
+    for eng in (0, 2):
+        for sch in (0, 1):
+            assert_same(ctx, nl, st, 61000, engine=eng, scheduler=sch, chunk_events=1 << 20, hashes=False)
