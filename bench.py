@@ -38,7 +38,7 @@ from paper_2304_13398_b200 import workloads as W  # noqa: E402
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
 
 # prefix of the workload the oracle runs (cycles), sized for ~10-30 s of one core
-SAMPLE_CYCLES = {"c4_10m": 3000, "c3_1m": 60, "c7552": 1999, "c5_set": 150}
+SAMPLE_CYCLES = {"c4_10m": 3000, "c3_1m": 60, "c7552": 1999, "c5_set": 150, "c4_mini": 3000}
 
 
 def parse():
@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--chunk-events", type=int, default=0)
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--arena-gb", type=float, default=0.0)
+    ap.add_argument("--engine", type=int, default=0)
+    ap.add_argument("--scheduler", type=int, default=0)
     return ap.parse_args()
 
 
@@ -209,7 +211,7 @@ def run_gls(a):
     stream = torch.cuda.current_stream(dev)
     ctx = gls.Context(local, stream.cuda_stream)
     ctx.gls_set_config(chunk_events=a.chunk_events, blocks_per_sm=a.blocks_per_sm,
-                       arena_bytes=int(a.arena_gb * (1 << 30)))
+                       arena_bytes=int(a.arena_gb * (1 << 30)), engine=a.engine, scheduler=a.scheduler)
     t = time.perf_counter()
     ctx.load(nl)
     L = ctx.gls_get_levels()
@@ -240,6 +242,8 @@ def run_gls(a):
         s = ctx.gls_get_stats()
         log(f"warmup {i}: kernel {s['kernel_ms']:.1f} ms, {s['gate_evals']} gate-evals, "
             f"{s['out_transitions']} outputs, {s['chunks']} chunks ({s['deep_chunks']} fallback), "
+            f"lane util {s['lane_utilization']:.2f}, batches {s['batches']} x {s['batch_lanes']:.1f} lanes / "
+            f"{s['batch_est']:.0f} est, phases {[round(x / max(1.0, sum(s['phase_cycles'])), 3) for x in s['phase_cycles']]}, "
             f"arena {s['arena_used_bytes'] / 1e9:.1f} GB "
             f"(wall {time.perf_counter() - t:.2f}s)")
     if world > 1:

@@ -111,6 +111,12 @@ typedef struct gls_stats {
                                 (DESIGN.md §7): 8·Σ fan-in reads + 8·outputs +
                                 20·pins + 8·gates                                  */
     int64_t fanin_reads;     /* Σ over pins of the driving net's transitions      */
+    double lane_utilization; /* slice engine: busy lane-iterations / occupied lane slots */
+    int64_t batches;         /* slice engine: warp batches                          */
+    double batch_lanes;      /* slice engine: mean lanes holding work per batch     */
+    double batch_est;        /* slice engine: mean expected transitions per batch   */
+    double phase_cycles[5];  /* slice engine, summed over warps: waiting + batch assembly,
+                                slice setup, slice loops, output copy, chunk completion */
     double kernel_ms;        /* CUDA-event time of the gate-evaluation kernel      */
     double simulate_ms;      /* CUDA-event time of the whole gls_simulate          */
 } gls_stats;

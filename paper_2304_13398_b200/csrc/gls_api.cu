@@ -137,6 +137,7 @@ struct gls_ctx {
     DevBuf<uint8_t> d_lut;
     DevBuf<uint32_t> d_perm;
     DevBuf<uint32_t> d_net_ck, d_net_nck, d_gate_done;
+    DevBuf<unsigned long long> d_gate_nin;
     DevBuf<unsigned long long> d_net_len;
     DevBuf<unsigned long long> d_work;
 
@@ -223,6 +224,7 @@ SimParams params(gls_ctx* ctx) {
     p.ck_gate = ctx->d_ck_gate.p;
     p.ck_cap = ctx->d_ck_T.n;
     p.gate_done = ctx->d_gate_done.p;
+    p.gate_nin = ctx->d_gate_nin.p;
     p.work = ctx->d_work.p;
     p.deep = ctx->d_deep.p;
     p.wscr = ctx->d_wscr.p;
@@ -501,6 +503,7 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
     CK(ctx->d_net_nck.alloc(N));
     CK(ctx->d_net_len.alloc(N));
     CK(ctx->d_gate_done.alloc(G));
+    CK(ctx->d_gate_nin.alloc(G));
     CK(ctx->d_work.alloc(L + 1));
     CK(ctx->d_fo_off.alloc(N + 1));
     CK(ctx->d_fo_gate.alloc(std::max<int64_t>(E, 1)));
@@ -690,6 +693,11 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
         s.levels = ctx->L;
         s.arena_used_bytes = (int64_t)c.arena_top * 8;
         s.kernel_ms = ms_k;
+        s.lane_utilization = c.warp_iters ? (double)c.lane_iters / (double)c.warp_iters : 0.0;
+        s.batches = (int64_t)c.batches;
+        s.batch_lanes = c.batches ? (double)c.batch_lanes / (double)c.batches : 0.0;
+        s.batch_est = c.batches ? (double)c.batch_est / (double)c.batches : 0.0;
+        for (int q = 0; q < 5; ++q) s.phase_cycles[q] = (double)c.cyc[q];
         s.simulate_ms = ms_s;
         s.alg_bytes = -1;  // computed on demand by gls_get_stats
         ctx->has_result = true;

@@ -55,6 +55,12 @@ struct Ctl {
     unsigned long long out_trans;
     unsigned long long chunks;
     unsigned long long deep_chunks;
+    unsigned long long lane_iters;    // slice engine: loop iterations summed over lanes
+    unsigned long long warp_iters;    // slice engine: 32 x the longest lane's iterations, summed over chunks
+    unsigned long long batches;       // slice engine: warp batches
+    unsigned long long batch_lanes;   // slice engine: lanes holding work, summed over batches
+    unsigned long long batch_est;     // slice engine: expected transitions, summed over batches
+    unsigned long long cyc[5];        // slice engine, lane 0 clocks: wait/assemble, setup, run, output, complete
 };
 
 struct SimParams {
@@ -77,6 +83,7 @@ struct SimParams {
     uint32_t* ck_gate;          // [ck_cap] internal gate of the chunk
     unsigned long long ck_cap;
     uint32_t* gate_done;        // [G] finished chunks per gate
+    unsigned long long* gate_nin;   // [G] Σ fan-in transitions (set when the gate is planned)
     unsigned long long* work;   // [L+1] per-level work counters
     uint64_t* deep;             // deep-backtrace scratch: one region per warp
     uint64_t* wscr;             // per-warp output scratch

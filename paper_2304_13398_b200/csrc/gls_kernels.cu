@@ -376,6 +376,7 @@ __device__ void plan_level(const SimParams& p, int l, unsigned gwarp, unsigned n
             if (c < 1) c = 1;
             if (c > lenref + 1) c = lenref + 1;
             nch = (unsigned)c;
+            p.gate_nin[gi] = n_in;
         }
         unsigned incl = warp_incl_scan(nch);
         unsigned total = __shfl_sync(0xffffffffu, incl, 31);
@@ -394,6 +395,19 @@ __device__ void plan_level(const SimParams& p, int l, unsigned gwarp, unsigned n
             p.net_ck[p.P + gi] = (uint32_t)my;
             p.net_nck[p.P + gi] = nch;
             p.gate_done[gi] = 0;
+            // chunk start times: quantiles of the longest fan-in's transition times
+            const GateInfo g = p.gate[gi];
+            unsigned long long lenref = 0;
+            uint32_t ref = 0;
+            for (uint32_t i = 0; i < g.k; ++i) {
+                const uint32_t src = p.pin_src[g.pin_off + i];
+                const unsigned long long len = p.net_len[src];
+                if (len > lenref) { lenref = len; ref = src; }
+            }
+            for (unsigned c = 0; c < nch; ++c) {
+                const unsigned long long q = lenref / nch, rm = lenref % nch;
+                p.ck_T[my + c] = c == 0 ? 0 : time_at(p, ref, (unsigned long long)c * q + ((unsigned long long)c * rm) / nch);
+            }
         }
         // the warp writes the chunk -> gate map of its 32 gates cooperatively
         for (int j = 0; j < 32; ++j) {
@@ -442,8 +456,9 @@ __device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetu
         unsigned long long q = lenref / nch, rm = lenref % nch;
         return (unsigned long long)cc * q + ((unsigned long long)cc * rm) / nch;
     };
-    s.T0 = c == 0 ? 0 : time_at(p, ref, qidx(c));
-    s.T1 = c + 1 == nch ? p.duration + 1 : time_at(p, ref, qidx(c + 1));
+    // chunk start times are written when the gate is planned (plan_gate / plan_level)
+    s.T0 = __ldcg(&p.ck_T[id]);
+    s.T1 = c + 1 == nch ? p.duration + 1 : __ldcg(&p.ck_T[id + 1]);
     if (q0_out) *q0_out = qidx(c);
     if (q1_out) *q1_out = c + 1 == nch ? lenref : qidx(c + 1);
     if (ref_out) *ref_out = ref;
@@ -602,8 +617,12 @@ __device__ __noinline__ void lane_chunk(const SimParams& p, const ChunkSetup& s,
 __device__ void plan_gate(const SimParams& p, uint32_t c) {
     const int lane = threadIdx.x & 31;
     const GateInfo g = p.gate[c];
-    const unsigned long long len = (uint32_t)lane < g.k ? __ldcg(&p.net_len[p.pin_src[g.pin_off + lane]]) : 0ull;
+    const uint32_t my_src = (uint32_t)lane < g.k ? p.pin_src[g.pin_off + lane] : 0u;
+    const unsigned long long len = (uint32_t)lane < g.k ? __ldcg(&p.net_len[my_src]) : 0ull;
     const unsigned long long n_in = warp_sum64(len), lenref = warp_max64(len);
+    // longest fan-in (first such pin): its quantiles are the chunk boundaries
+    const unsigned bm = __ballot_sync(0xffffffffu, (uint32_t)lane < g.k && len == lenref);
+    const uint32_t ref = __shfl_sync(0xffffffffu, my_src, __ffs(bm) - 1);
     unsigned long long nch = (n_in + (unsigned long long)p.M - 1) / (unsigned long long)p.M;
     if (nch < 1) nch = 1;
     if (nch > lenref + 1) nch = lenref + 1;
@@ -620,9 +639,16 @@ __device__ void plan_gate(const SimParams& p, uint32_t c) {
     if (lane == 0) {
         p.net_ck[p.P + c] = (uint32_t)base;
         p.net_nck[p.P + c] = (uint32_t)nch;
+        p.gate_nin[c] = n_in;
         p.gate_done[c] = 0;
         fence_release();
     }
+    // chunk start times: quantiles of the longest fan-in's transition times
+    for (unsigned long long j = lane; j < nch; j += 32) {
+        const unsigned long long q = lenref / nch, rm = lenref % nch;
+        p.ck_T[base + j] = j == 0 ? 0 : time_at(p, ref, j * q + (j * rm) / nch);
+    }
+    fence_release();
     __syncwarp();
     for (unsigned long long j = lane; j < nch; j += 32) st_relaxed_u32(&p.ck_gate[base + j], c);
 }
@@ -742,13 +768,9 @@ namespace gls {
 constexpr int kDtabWords = 24;   // per-thread delay table words (slice engine)
 constexpr unsigned kEmpty = 0xffffffffu;
 
-template <int ENGINE>
-__device__ __forceinline__ void process_one(const SimParams& p, unsigned long long id, const uint8_t* lut,
-                                            unsigned char* s_dyn, ChunkResult& R) {
-    if (ENGINE == 0)
-        sl::process_chunk_slice(p, id, lut, reinterpret_cast<uint32_t*>(s_dyn), R);
-    else
-        process_chunk_warp(p, id, lut, reinterpret_cast<wv::WS*>(s_dyn)[threadIdx.x >> 5], R);
+// slice engine shared memory: per-thread delay tables, then one Batch per warp
+__device__ __forceinline__ sl::Batch& slice_batch_smem(unsigned char* s_dyn) {
+    return reinterpret_cast<sl::Batch*>(s_dyn + (size_t)kDtabWords * kThreads * 4)[threadIdx.x >> 5];
 }
 
 template <int ENGINE, bool DATAFLOW>
@@ -764,6 +786,12 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
     if (DATAFLOW) {
         // seed: gates fed only by given nets (topological level 1) are ready now
         for (int g = (int)gwarp; g < p.level_off[1]; g += (int)nwarps) plan_gate(p, (uint32_t)g);
+        if (ENGINE == 0) {
+            unsigned long long carry = ~0ull;
+            while (sl::slice_batch<true>(p, s_lut, reinterpret_cast<uint32_t*>(s_dyn), slice_batch_smem(s_dyn),
+                                         carry, 0, 0, nullptr)) {
+            }
+        } else {
         // pull published chunks until every gate is complete (Alg. 1 loop)
         for (;;) {
             unsigned long long id = 0;
@@ -790,7 +818,7 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
                         break;
                     }
                     __nanosleep(ns);
-                    if (ns < 1024) ns <<= 1;
+                    if (ns < 8192) ns <<= 1;
                 }
                 p.deep_wtop[gwarp] = 0;                 // this warp's deep scratch, reused per chunk
             }
@@ -799,8 +827,9 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
             if (g == kEmpty) return;
             __syncwarp();
             ChunkResult R;
-            process_one<ENGINE>(p, id, s_lut, s_dyn, R);
+            process_chunk_warp(p, id, s_lut, reinterpret_cast<wv::WS*>(s_dyn)[threadIdx.x >> 5], R);
             chunk_done<true>(p, id, R);
+        }
         }
     } else {
         unsigned gen = 0;
@@ -811,6 +840,11 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
             const unsigned long long ck_end = *(volatile unsigned long long*)&p.ctl->chunk_top;
             if (ENGINE == 1) {
                 process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
+            } else if (ENGINE == 0) {
+                unsigned long long carry = ~0ull;
+                while (sl::slice_batch<false>(p, s_lut, reinterpret_cast<uint32_t*>(s_dyn), slice_batch_smem(s_dyn),
+                                              carry, ck_begin, ck_end - ck_begin, &p.work[l])) {
+                }
             } else {
                 const unsigned long long n = ck_end - ck_begin;
                 for (;;) {
@@ -823,7 +857,7 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
                     if (wb >= n) break;
                     __syncwarp();
                     ChunkResult R;
-                    process_one<ENGINE>(p, ck_begin + wb, s_lut, s_dyn, R);
+                    process_chunk_warp(p, ck_begin + wb, s_lut, reinterpret_cast<wv::WS*>(s_dyn)[threadIdx.x >> 5], R);
                     chunk_done<false>(p, ck_begin + wb, R);
                 }
             }
@@ -921,7 +955,8 @@ __global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long 
 
 // ------------------------------------------------------------------ launchers
 static size_t dyn_smem(int engine) {
-    return engine == 2 ? wv::kSmemBytes : (engine == 0 ? (size_t)kDtabWords * kThreads * 4 : 0);
+    return engine == 2 ? wv::kSmemBytes
+                       : (engine == 0 ? (size_t)kDtabWords * kThreads * 4 + sl::kBatchBytes * (kThreads / 32) : 0);
 }
 static const void* kernel_for(int engine, int sched) {
     if (engine == 1) return (const void*)sim_kernel<1, false>;

@@ -19,7 +19,7 @@ namespace gls {
 namespace sl {
 
 constexpr int RD = 4;                  // register pending ring depth
-constexpr int LCAP = 256;              // per-lane output scratch entries
+constexpr int LCAP = 1024;             // per-lane output scratch entries
 constexpr int E_MIN = 32;              // fewest expected transitions per lane
 constexpr unsigned FULL = 0xffffffffu;
 constexpr size_t kScratchPerWarp = 32u * LCAP;
@@ -51,7 +51,8 @@ __device__ __noinline__ Seg next_segment(const SimParams& p, uint32_t ck, uint32
 template <bool DIRECT>
 __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s, const uint8_t* lut,
                                          const uint32_t* dtab, int dstride, uint64_t* out, uint32_t& cnt,
-                                         uint32_t& vb, uint32_t& evals, uint32_t& events) {
+                                         uint32_t& vb, uint32_t& evals, uint32_t& events, uint32_t& iters,
+                                         uint32_t cap) {
     Cur c[4];
     uint64_t h[4];
     uint32_t xn = 0, x0 = 0;
@@ -89,7 +90,7 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
         if (r < T0) {
             vb = (uint32_t)(e & 3u);
         } else if (r < T1 && r <= dur) {
-            if (DIRECT || n_out < (uint32_t)LCAP) out[n_out] = e;
+            if (DIRECT || n_out < cap) out[n_out] = e;
             ++n_out;
         }
         lastv = (uint32_t)(e & 3u);
@@ -138,7 +139,9 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
     };
 
     step(s.tau0, x0);                                   // the slice's halo start
+    uint32_t n_it = 0;
     for (;;) {
+        ++n_it;
         const uint64_t m = min(min(h[0], h[1]), min(h[2], h[3]));
         if (m >= lim1 || status) break;
         const long long t = etime(m);
@@ -169,63 +172,253 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
     cnt = n_out;
     evals = n_evals;
     events = n_ev;
-    if (!DIRECT && status == 0 && n_out > (uint32_t)LCAP) status = 2;
+    iters = n_it;
+    if (!DIRECT && status == 0 && n_out > cap) status = 2;
     return status;
 }
 
-// One chunk with the slice engine (whole warp).
-__device__ void process_chunk_slice(const SimParams& p, unsigned long long id, const uint8_t* lut, uint32_t* s_dtab,
-                                    ChunkResult& R) {
-    const int lane = threadIdx.x & 31;
-    uint64_t* scr = p.wscr + (size_t)warp_global_id() * kScratchPerWarp;
-    uint32_t* dtab = s_dtab + threadIdx.x;              // [q * blockDim.x + tid]
-    const int dstride = (int)blockDim.x;
-    ChunkSetup& s = R.s;
-    unsigned long long q0 = 0, q1 = 0, n_in = 0;
-    uint32_t ref = 0, cidx = 0;
-    setup_chunk(p, id, s, R.gi, cidx, R.nch, &q0, &q1, &ref, &n_in);
-    // lanes and slice boundaries (quantiles of the longest fan-in inside the chunk)
-    const unsigned long long span = q1 - q0;
-    const unsigned long long lenref = __ldcg(&p.net_len[ref]);
-    const double est = lenref ? (double)span * (double)n_in / (double)lenref : 0.0;
-    int nl = (int)fmin(32.0, fmax(1.0, est / (double)E_MIN));
-    if ((unsigned long long)nl > span) nl = (int)max(1ull, span);
-    long long Tl = s.T0;
-    if (lane > 0 && lane < nl) {
-        const unsigned long long qi = q0 + (span * (unsigned long long)lane) / (unsigned long long)nl;
-        Tl = time_at(p, ref, qi);
+// Per-warp batch (lane 0 assembles it from the chunk queue): published chunks
+// are claimed until the batch holds about 32 x W_LANE expected transitions;
+// then the 32 lanes are spread in proportion to the expected work w = total/32:
+// a chunk with at least w gets about est/w lanes, one time slice each (cut at
+// quantiles of its longest fan-in); smaller chunks are packed whole, several
+// per lane.  Units are assigned in lane order, so the slices of a chunk sit on
+// consecutive lanes and a lane's units are contiguous.
+constexpr int W_LANE = 128;            // a batch is filled up to 32 x W_LANE expected transitions
+constexpr int W_MIN = 32;              // fewest expected transitions per lane (slice setup cost)
+constexpr int MAXC = 96;               // chunks per batch
+constexpr int MAXU = 160;              // units per batch
+struct Batch {
+    unsigned long long id[MAXC];
+    uint8_t nsl[MAXC];                     // slices of the chunk
+    uint8_t first_unit[MAXC];
+    uint8_t u_chunk[MAXU], u_slice[MAXU];  // unit -> (chunk, slice)
+    uint8_t lane_u0[32], lane_nu[32];      // lane -> its units [u0, u0 + nu)
+    uint32_t u_cnt[MAXU], u_ev[MAXU], u_evt[MAXU];
+    uint16_t u_soff[MAXU];                 // offset of the unit's outputs in its lane scratch
+    uint32_t u_pre[MAXU];                  // offset of the unit's outputs inside its chunk
+    uint8_t u_vb[MAXU], u_st[MAXU], u_lane[MAXU];
+    unsigned long long c_off[MAXC];
+    long long c_T0[MAXC];                  // chunk start time (recorded by its slice 0)
+    uint32_t c_total[MAXC];
+};
+constexpr size_t kBatchBytes = sizeof(Batch);
+
+// this unit's time range: the chunk, or one slice of it (quantiles of the
+// longest fan-in inside the chunk); each slice is an exact chunk
+// (the slice's end is the next slice's start: computed by the next lane when it
+// is that slice's lane, else here)
+__device__ __forceinline__ long long slice_start(const SimParams& p, uint32_t ref, unsigned long long q0,
+                                                 unsigned long long q1, int sidx, int nsl, long long T0) {
+    return sidx == 0 ? T0 : time_at(p, ref, q0 + ((q1 - q0) * (unsigned long long)sidx) / nsl);
+}
+__device__ __forceinline__ void unit_setup(const SimParams& p, unsigned long long id, int sidx, int nsl,
+                                           ChunkSetup& s, uint32_t& gi, uint32_t& nch, const long long* next_start) {
+    uint32_t cidx, ref;
+    unsigned long long q0, q1, n_in;
+    setup_chunk(p, id, s, gi, cidx, nch, &q0, &q1, &ref, &n_in);
+    if (nsl > 1) {
+        const long long t0 = slice_start(p, ref, q0, q1, sidx, nsl, s.T0);
+        const long long t1 = sidx + 1 == nsl ? s.T1
+                             : next_start ? *next_start
+                                          : slice_start(p, ref, q0, q1, sidx + 1, nsl, s.T0);
+        s.T0 = t0;
+        s.T1 = t1;
+        s.tau0 = t0 - (long long)s.dmax - 1;
     }
-    const long long Tn0 = __shfl_down_sync(FULL, Tl, 1);
-    const long long Tn = lane + 1 < nl ? Tn0 : s.T1;
-    uint32_t cnt = 0, vb = 2, ev = 0, evt = 0;
-    int st = 0;
-    ChunkSetup ls = s;
-    ls.T0 = Tl;
-    ls.T1 = Tn;
-    ls.tau0 = Tl - (long long)s.dmax - 1;
-    if (lane < nl) {
-        // this lane's delay table (R1: output X takes the smaller delay)
+}
+__device__ __forceinline__ void fill_dtab(uint32_t* dtab, int dstride, const ChunkSetup& s) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint4 d = s.d[i];
-            dtab[(i * 6 + 0) * dstride] = d.z;
-            dtab[(i * 6 + 1) * dstride] = d.w;
-            dtab[(i * 6 + 2) * dstride] = min(d.z, d.w);
-            dtab[(i * 6 + 3) * dstride] = d.x;
-            dtab[(i * 6 + 4) * dstride] = d.y;
-            dtab[(i * 6 + 5) * dstride] = min(d.x, d.y);
+    for (int i = 0; i < 4; ++i) {                       // R1: output X takes the smaller delay
+        const uint4 d = s.d[i];
+        dtab[(i * 6 + 0) * dstride] = d.z;
+        dtab[(i * 6 + 1) * dstride] = d.w;
+        dtab[(i * 6 + 2) * dstride] = min(d.z, d.w);
+        dtab[(i * 6 + 3) * dstride] = d.x;
+        dtab[(i * 6 + 4) * dstride] = d.y;
+        dtab[(i * 6 + 5) * dstride] = min(d.x, d.y);
+    }
+}
+
+// Whole warp: evaluate one batch.  Returns false when there is no more work
+// (dataflow: every gate done or an error; levels: the level is exhausted).
+// `carry` (lane 0) holds a claimed chunk id that did not fit the last batch.
+template <bool DATAFLOW>
+__device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_dtab, Batch& B,
+                            unsigned long long& carry, unsigned long long lvl_begin, unsigned long long lvl_n,
+                            unsigned long long* lvl_work) {
+    const int lane = threadIdx.x & 31;
+    constexpr unsigned long long NONE = ~0ull;
+    int nc = 0, nu = 0;
+    bool more = true;
+    const long long c_start = clock64();
+    if (lane == 0) {
+        // phase 1: claim published chunks until the batch holds about 32 x W_LANE transitions
+        unsigned long long est[MAXC];
+        unsigned long long total = 0;
+        while (nc < MAXC && total < 32ull * W_LANE) {
+            unsigned long long id;
+            if (carry != NONE) {
+                id = carry;
+                carry = NONE;
+            } else if (DATAFLOW) {
+                id = atomicAdd(&p.ctl->work_head, 1ull);
+            } else {
+                const unsigned long long w = atomicAdd(lvl_work, 1ull);
+                if (w >= lvl_n) break;
+                id = lvl_begin + w;
+            }
+            uint32_t g;
+            if (DATAFLOW) {
+                g = id < p.ck_cap ? ld_relaxed_u32(&p.ck_gate[id]) : 0xffffffffu;
+                if (g == 0xffffffffu) {
+                    if (nc > 0) {                           // never wait while holding work
+                        carry = id;
+                        break;
+                    }
+                    unsigned ns = 32;
+                    unsigned long long t_start = 0, seen = ~0ull;
+                    for (;;) {
+                        if (id < p.ck_cap) {
+                            g = ld_relaxed_u32(&p.ck_gate[id]);
+                            if (g != 0xffffffffu) break;
+                        }
+                        const unsigned long long done = ld_relaxed_u64(&p.ctl->done_gates);
+                        if (done >= (unsigned long long)p.G || ld_relaxed_u32(&p.ctl->error) != 0u) break;
+                        unsigned long long now;             // watchdog (10 s without progress)
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                        if (done != seen) {
+                            seen = done;
+                            t_start = now;
+                        } else if (now - t_start > 10000000000ull) {
+                            atomicOr(&p.ctl->error, kErrWatchdog);
+                            break;
+                        }
+                        __nanosleep(ns);
+                        if (ns < 8192) ns <<= 1;
+                    }
+                    if (g == 0xffffffffu) {
+                        more = false;
+                        break;
+                    }
+                }
+            } else {
+                g = __ldcg(&p.ck_gate[id]);
+            }
+            const unsigned long long nch = __ldcg(&p.net_nck[p.P + g]);
+            const unsigned long long e = __ldcg(&p.gate_nin[g]) / (nch ? nch : 1ull);
+            B.id[nc] = id;
+            est[nc] = e;
+            total += e;
+            ++nc;
         }
-        st = run_slice<false>(p, ls, lut, dtab, dstride, scr + (size_t)lane * LCAP, cnt, vb, ev, evt);
+        if (nc > 0) {
+            atomicAdd(&p.ctl->batches, 1ull);
+            atomicAdd(&p.ctl->batch_est, total);
+        }
+        // phase 2: spread the 32 lanes in proportion to the expected work (w per lane)
+        const unsigned long long w = max((unsigned long long)W_MIN, (total + 31) / 32);
+        int next_lane = 0, shared = -1;
+        unsigned long long shared_load = 0;
+        for (int q = 0; q < 32; ++q) B.lane_nu[q] = 0;
+        for (int j = 0; j < nc; ++j) {
+            const unsigned long long e = est[j];
+            const int left = 32 - next_lane;
+            B.first_unit[j] = (uint8_t)nu;
+            if (e >= w && left > 0 && nu + left <= MAXU) {
+                const int ns = (int)min((unsigned long long)left, max(1ull, (e + w / 2) / w));
+                B.nsl[j] = (uint8_t)ns;
+                for (int q = 0; q < ns; ++q) {
+                    B.u_chunk[nu] = (uint8_t)j;
+                    B.u_slice[nu] = (uint8_t)q;
+                    B.u_lane[nu] = (uint8_t)next_lane;
+                    B.lane_u0[next_lane] = (uint8_t)nu;
+                    B.lane_nu[next_lane] = 1;
+                    ++next_lane;
+                    ++nu;
+                }
+                shared = -1;                        // a lane's units must stay contiguous
+            } else {
+                if (shared < 0 || (shared_load + e > w && left > 0)) {
+                    if (left > 0) {
+                        shared = next_lane++;
+                        shared_load = 0;
+                        B.lane_u0[shared] = (uint8_t)nu;
+                    } else {
+                        shared = 31;                // out of lanes: the last lane takes the rest
+                    }
+                }
+                B.nsl[j] = 1;
+                B.u_chunk[nu] = (uint8_t)j;
+                B.u_slice[nu] = 0;
+                B.u_lane[nu] = (uint8_t)shared;
+                B.lane_nu[shared]++;
+                shared_load += e;
+                ++nu;
+            }
+        }
+        if (nc > 0) {
+            int busy = 0;
+            for (int q = 0; q < 32; ++q) busy += B.lane_nu[q] > 0;
+            atomicAdd(&p.ctl->batch_lanes, (unsigned long long)busy);
+        }
+        p.deep_wtop[warp_global_id()] = 0;          // this warp's deep scratch, reused per batch
+    }
+    nc = __shfl_sync(FULL, nc, 0);
+    more = __shfl_sync(FULL, (int)more, 0) != 0;
+    __syncwarp();
+    if (nc == 0) return DATAFLOW ? more : false;
+    nu = __shfl_sync(FULL, nu, 0);
+
+    uint64_t* const wscr = p.wscr + (size_t)warp_global_id() * kScratchPerWarp;
+    uint64_t* scr = wscr + (size_t)lane * LCAP;
+    uint32_t* dtab = s_dtab + threadIdx.x;                // [q * blockDim.x + tid]
+    const int dstride = (int)blockDim.x;
+    // ---- each lane: its units, in order
+    const int u0 = B.lane_u0[lane], nun = B.lane_nu[lane];
+    uint32_t used = 0, its_sum = 0;
+    const long long c_asm = clock64();
+    long long c_setup = 0;
+    // a slice lane (one unit, of a chunk with several slices) publishes its start time to
+    // the previous lane, whose slice ends there
+    long long my_start = 0;
+    bool slice_lane = false;
+    if (nun == 1 && B.nsl[B.u_chunk[u0]] > 1) {
+        const int j = B.u_chunk[u0];
+        ChunkSetup s0;
+        uint32_t gi0, cidx0, nch0, ref0;
+        unsigned long long q0, q1, nin0;
+        setup_chunk(p, B.id[j], s0, gi0, cidx0, nch0, &q0, &q1, &ref0, &nin0);
+        my_start = slice_start(p, ref0, q0, q1, B.u_slice[u0], B.nsl[j], s0.T0);
+        slice_lane = true;
+    }
+    const long long nb_start = __shfl_down_sync(FULL, my_start, 1);
+    const bool nb_same = __shfl_down_sync(FULL, (int)(slice_lane ? (int)B.u_chunk[u0] : -1), 1) ==
+                         (slice_lane ? (int)B.u_chunk[u0] : -2);
+    for (int u = u0; u < u0 + nun; ++u) {
+        const long long c_us = clock64();
+        const int j = B.u_chunk[u];
+        ChunkSetup s;
+        uint32_t gi, nch;
+        unit_setup(p, B.id[j], B.u_slice[u], B.nsl[j], s, gi, nch,
+                   (slice_lane && nb_same && lane < 31) ? &nb_start : nullptr);
+        if (B.u_slice[u] == 0) B.c_T0[j] = s.T0;
+        fill_dtab(dtab, dstride, s);
+        c_setup += clock64() - c_us;
+        uint32_t cnt = 0, vb = 2, ev = 0, evt = 0, its = 0;
+        const uint32_t cap = used < (uint32_t)LCAP ? (uint32_t)LCAP - used : 0u;
+        int st = run_slice<false>(p, s, lut, dtab, dstride, scr + (used < (uint32_t)LCAP ? used : 0u), cnt, vb,
+                                  ev, evt, its, cap);
         if (st == 1) {
-            // pending ring overflow: exact count of the slice by the per-lane engine (deep ring if needed)
+            // pending ring overflow: exact count by the per-lane engine (deep ring if needed)
             ChunkOut r{0, 0, 0, 2, false};
-            run_chunk<false, false>(p, ls, lut, nullptr, nullptr, 0, r);
+            run_chunk<false, false>(p, s, lut, nullptr, nullptr, 0, r);
             if (r.overflow) {
-                const unsigned long long dcap = window_bound(p, ls);
+                const unsigned long long dcap = window_bound(p, s);
                 const unsigned long long at = deep_alloc(p, dcap);
                 if (at != ~0ull) {
                     r = ChunkOut{0, 0, 0, 2, false};
-                    run_chunk<false, true>(p, ls, lut, nullptr, p.deep + at, dcap, r);
+                    run_chunk<false, true>(p, s, lut, nullptr, p.deep + at, dcap, r);
                 }
             }
             cnt = r.cnt;
@@ -233,50 +426,126 @@ __device__ void process_chunk_slice(const SimParams& p, unsigned long long id, c
             ev = r.evals;
             evt = r.events;
         }
+        if (st != 0) atomicAdd(&p.ctl->deep_chunks, 1ull);
+        B.u_cnt[u] = cnt;
+        B.u_ev[u] = ev;
+        B.u_evt[u] = evt;
+        B.u_vb[u] = (uint8_t)vb;
+        B.u_st[u] = (uint8_t)st;
+        B.u_soff[u] = (uint16_t)(used < (uint32_t)LCAP ? used : 0u);
+        if (st == 0) used += cnt;
+        its_sum += its;
     }
-    if (lane < nl && st != 0) atomicAdd(&p.ctl->deep_chunks, 1ull);
-    uint32_t pre = cnt;
+    __syncwarp();
+    const long long c_run = clock64();
+    {   // lane utilisation counters
+        const unsigned long long sum_it = warp_sum64(its_sum);
+        unsigned long long mx = its_sum;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t a = __shfl_up_sync(FULL, pre, o);
-        if (lane >= o) pre += a;
-    }
-    const uint32_t total = __shfl_sync(FULL, pre, 31);
-    pre -= cnt;
-    const unsigned long long off = arena_alloc(p, total);
-    R.fits = off != ~0ull;
-    if (R.fits) {
-        const unsigned clean = __ballot_sync(FULL, st == 0);
-        for (int j = 0; j < nl; ++j) {                    // coalesced copy-out, lane by lane
-            if (!((clean >> j) & 1u)) continue;
-            const uint32_t cj = __shfl_sync(FULL, cnt, j);
-            const uint32_t pj = __shfl_sync(FULL, pre, j);
-            const uint64_t* src = scr + (size_t)j * LCAP;
-            for (uint32_t q = lane; q < cj; q += 32) p.arena[off + pj + q] = src[q];
+        for (int o = 16; o > 0; o >>= 1) mx = max(mx, (unsigned long long)__shfl_xor_sync(FULL, mx, o));
+        if (lane == 0) {
+            atomicAdd(&p.ctl->lane_iters, sum_it);
+            atomicAdd(&p.ctl->warp_iters, 32ull * mx);
         }
-        if (lane < nl && st == 2) {                       // scratch overflow: re-run straight into place
-            uint32_t c2, v2, e2, t2;
-            run_slice<true>(p, ls, lut, dtab, dstride, p.arena + off + pre, c2, v2, e2, t2);
-            if (c2 != cnt) atomicOr(&p.ctl->error, kErrBug);
-        } else if (lane < nl && st == 1) {                 // ring overflow: per-lane engine writes in place
+    }
+    __syncwarp();
+    // ---- per chunk: unit offsets, total and one exact segment
+    for (int j = lane; j < nc; j += 32) {
+        uint32_t tot = 0;
+        for (int u = B.first_unit[j]; u < B.first_unit[j] + B.nsl[j]; ++u) {
+            B.u_pre[u] = tot;
+            tot += B.u_cnt[u];
+        }
+        unsigned long long off = tot ? atomicAdd(&p.ctl->arena_top, seg_round(tot)) : 0ull;
+        if (off + tot > p.arena_cap) {
+            atomicOr(&p.ctl->error, kErrArena);
+            atomicMax(&p.ctl->need_arena, off + tot);
+            off = ~0ull;
+        }
+        B.c_off[j] = off;
+        B.c_total[j] = tot;
+    }
+    __syncwarp();
+    // ---- each lane moves its clean units into place (independent loads, overlapped latency)
+    for (int u = u0; u < u0 + nun; ++u) {
+        const unsigned long long off = B.c_off[B.u_chunk[u]];
+        const uint32_t cu = B.u_cnt[u];
+        if (off == ~0ull || B.u_st[u] != 0 || cu == 0) continue;
+        const uint64_t* src = scr + B.u_soff[u];
+        uint64_t* dst = p.arena + off + B.u_pre[u];
+        uint32_t e = 0;
+        for (; e + 4 <= cu; e += 4) {
+            const uint64_t a0 = src[e], a1 = src[e + 1], a2 = src[e + 2], a3 = src[e + 3];
+            dst[e] = a0;
+            dst[e + 1] = a1;
+            dst[e + 2] = a2;
+            dst[e + 3] = a3;
+        }
+        for (; e < cu; ++e) dst[e] = src[e];
+    }
+    // ---- units whose scratch or ring overflowed: the owning lane writes them in place
+    for (int u = u0; u < u0 + nun; ++u) {
+        const int st = B.u_st[u];
+        if (st == 0) continue;
+        const int j = B.u_chunk[u];
+        const unsigned long long off = B.c_off[j];
+        if (off == ~0ull) continue;
+        ChunkSetup s;
+        uint32_t gi, nch;
+        unit_setup(p, B.id[j], B.u_slice[u], B.nsl[j], s, gi, nch, nullptr);
+        fill_dtab(dtab, dstride, s);
+        uint64_t* dst = p.arena + off + B.u_pre[u];
+        if (st == 2) {                                  // scratch overflow: re-run straight into place
+            uint32_t c2, v2, e2, t2, i2;
+            run_slice<true>(p, s, lut, dtab, dstride, dst, c2, v2, e2, t2, i2, 0u);
+            if (c2 != B.u_cnt[u]) atomicOr(&p.ctl->error, kErrBug);
+        } else {                                        // ring overflow: per-lane engine in place
             ChunkOut r2{0, 0, 0, 2, false};
-            run_chunk<true, false>(p, ls, lut, p.arena + off + pre, nullptr, 0, r2);
+            run_chunk<true, false>(p, s, lut, dst, nullptr, 0, r2);
             if (r2.overflow) {
-                const unsigned long long dcap = window_bound(p, ls);
+                const unsigned long long dcap = window_bound(p, s);
                 const unsigned long long at = deep_alloc(p, dcap);
                 if (at != ~0ull) {
                     r2 = ChunkOut{0, 0, 0, 2, false};
-                    run_chunk<true, true>(p, ls, lut, p.arena + off + pre, p.deep + at, dcap, r2);
+                    run_chunk<true, true>(p, s, lut, dst, p.deep + at, dcap, r2);
                 }
             }
-            if (r2.cnt != cnt) atomicOr(&p.ctl->error, kErrBug);
+            if (r2.cnt != B.u_cnt[u]) atomicOr(&p.ctl->error, kErrBug);
         }
     }
-    R.off = off;
-    R.total = total;
-    R.vb = __shfl_sync(FULL, vb, 0);
-    R.evals = warp_sum64(ev);
-    R.events = warp_sum64(evt);
+    __syncwarp();
+    const long long c_out = clock64();
+    // ---- complete the chunks (whole warp, one after the other)
+    for (int j = 0; j < nc; ++j) {
+        const int ufirst = B.first_unit[j];
+        const unsigned long long id = B.id[j];
+        ChunkResult R;
+        R.gi = __ldcg(&p.ck_gate[id]);
+        R.nch = __ldcg(&p.net_nck[p.P + R.gi]);
+        R.s.T0 = B.c_T0[j];
+        R.off = B.c_off[j];
+        R.fits = R.off != ~0ull;
+        R.total = B.c_total[j];
+        R.vb = B.u_vb[ufirst];
+        unsigned long long e1 = 0, e2 = 0;
+        for (int u = ufirst; u < ufirst + B.nsl[j]; ++u) {
+            e1 += B.u_ev[u];
+            e2 += B.u_evt[u];
+        }
+        R.evals = e1;
+        R.events = e2;
+        chunk_done<DATAFLOW>(p, id, R);
+    }
+    const long long c_end = clock64();
+    const unsigned long long setup_max = warp_max64((unsigned long long)c_setup);
+    if (lane == 0) {
+        atomicAdd(&p.ctl->cyc[0], (unsigned long long)(c_asm - c_start));
+        atomicAdd(&p.ctl->cyc[1], setup_max);
+        atomicAdd(&p.ctl->cyc[2], (unsigned long long)(c_run - c_asm) - setup_max);
+        atomicAdd(&p.ctl->cyc[3], (unsigned long long)(c_out - c_run));
+        atomicAdd(&p.ctl->cyc[4], (unsigned long long)(c_end - c_out));
+    }
+    return true;
 }
 
 }  // namespace sl

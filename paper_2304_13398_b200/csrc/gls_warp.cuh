@@ -181,8 +181,8 @@ __device__ __forceinline__ void refill(const SimParams& p, WS& ws, int i, uint32
         if (rem == 0) {
             if (ck + 1 < ckend) {
                 ++ck;
-                off = p.ck_off[ck];
-                rem = p.ck_cnt[ck];
+                off = __ldcg(&p.ck_off[ck]);      // L2: never a stale L1 line (dataflow)
+                rem = __ldcg(&p.ck_cnt[ck]);
                 continue;
             }
             more = 0;

@@ -46,10 +46,15 @@ class gls_stats(ctypes.Structure):
                 ("deep_chunks", ctypes.c_int64), ("levels", ctypes.c_int64),
                 ("arena_used_bytes", ctypes.c_int64), ("alg_bytes", ctypes.c_int64),
                 ("fanin_reads", ctypes.c_int64),
-                ("kernel_ms", ctypes.c_double), ("simulate_ms", ctypes.c_double)]
+                ("lane_utilization", ctypes.c_double), ("batches", ctypes.c_int64),
+                ("batch_lanes", ctypes.c_double), ("batch_est", ctypes.c_double),
+                ("phase_cycles", ctypes.c_double * 5), ("kernel_ms", ctypes.c_double),
+                ("simulate_ms", ctypes.c_double)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["phase_cycles"] = list(self.phase_cycles)
+        return d
 
 
 _lib = None

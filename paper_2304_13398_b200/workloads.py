@@ -429,6 +429,9 @@ CONFIGS = {
     "c4_10m": dict(num_gates=10 * (1 << 20), depth=250, num_inputs=1 << 20, ncycles=297203,
                    profile="skewed", mean_trans=1000, wcv=17.0),
     "c5_set": dict(num_gates=1 << 20, depth=200, num_inputs=104858, ncycles=1999, profile="random"),
+    # C4's per-net activity and skew on 1/10 of the gates (profiling stand-in for C4)
+    "c4_mini": dict(num_gates=1 << 20, depth=100, num_inputs=104858, ncycles=297203,
+                    profile="skewed", mean_trans=1000, wcv=17.0),
 }
 
 
