@@ -197,6 +197,14 @@ def window_hash_numpy(offsets, trans, t_lo, t_hi):
     return out
 
 
+def balance_str(s):
+    """slice-engine lane balance: (within slice groups, slice lanes vs batch max, packed vs batch max, idle share)"""
+    b = s.get("balance") or [0] * 8
+    f = lambda x, y: round(x / y, 3) if y else 0.0
+    return (f"[slice-in-group {f(b[0], b[1])}, slice {f(b[0], b[4])}, packed {f(b[2], b[3])}, "
+            f"idle {f(b[5], b[3] + b[4] + b[5])}, lanes sl/pk {f(b[6], b[6] + b[7])}]")
+
+
 def run_gls(a):
     from paper_2304_13398_b200 import gls
     rank, world, local = dist_env()
@@ -244,7 +252,7 @@ def run_gls(a):
             f"{s['out_transitions']} outputs, {s['chunks']} chunks ({s['deep_chunks']} fallback), "
             f"lane util {s['lane_utilization']:.2f}, batches {s['batches']} x {s['batch_lanes']:.1f} lanes / "
             f"{s['batch_est']:.0f} est, phases {[round(x / max(1.0, sum(s['phase_cycles'])), 3) for x in s['phase_cycles']]}, "
-            f"arena {s['arena_used_bytes'] / 1e9:.1f} GB "
+            f"arena {s['arena_used_bytes'] / 1e9:.1f} GB, balance {balance_str(s)} "
             f"(wall {time.perf_counter() - t:.2f}s)")
     if world > 1:
         torch.distributed.barrier()

@@ -117,6 +117,12 @@ typedef struct gls_stats {
     double batch_est;        /* slice engine: mean expected transitions per batch   */
     double phase_cycles[5];  /* slice engine, summed over warps: waiting + batch assembly,
                                 slice setup, slice loops, output copy, chunk completion */
+    double balance[8];       /* slice engine lane-balance counters (loop iterations):
+                                [0] Σ over slice lanes, [1] Σ over slice lanes of their
+                                group's longest lane, [2] Σ over packed lanes, [3] Σ over
+                                packed lanes of the batch's longest lane, [4] Σ over slice
+                                lanes of the batch's longest lane, [5] Σ over idle lanes of
+                                the batch's longest lane, [6] slice lanes, [7] packed lanes */
     double kernel_ms;        /* CUDA-event time of the gate-evaluation kernel      */
     double simulate_ms;      /* CUDA-event time of the whole gls_simulate          */
 } gls_stats;

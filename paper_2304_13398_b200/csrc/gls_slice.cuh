@@ -18,6 +18,9 @@
 namespace gls {
 namespace sl {
 
+#ifndef GLS_PF
+#define GLS_PF 1
+#endif
 constexpr int RD = 4;                  // register pending ring depth
 constexpr int LCAP = 1024;             // per-lane output scratch entries
 constexpr int E_MIN = 32;              // fewest expected transitions per lane
@@ -76,10 +79,12 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
         }
     }
     const uint32_t lb = s.lut_base;
-    const long long T0 = s.T0, T1 = s.T1, dur = p.duration, dmin = (long long)s.dmin;
-    const uint64_t lim1 = (uint64_t)T1 << 2;           // entry time >= T1  <=>  entry >= lim1
+    const long long T0 = s.T0, T1 = s.T1, dmin = (long long)s.dmin;
+    const long long T1e = min(T1, p.duration + 1);     // outputs in [T0, T1) and <= duration (R7)
+    uint64_t lim1 = (uint64_t)T1 << 2;                 // entry time >= T1  <=>  entry >= lim1
     uint64_t rg0 = 0, rg1 = 0, rg2 = 0, rg3 = 0;       // pending ring: rg0 newest, rg[rn-1] oldest
     int rn = 0;
+    long long ft = LLONG_MAX;                          // time of the oldest pending entry (none: max)
     uint32_t Eprev = 2, lastv = 2;
     uint32_t n_out = 0, n_ev = 0, n_evals = 0;
     vb = 2;
@@ -89,13 +94,26 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
         const long long r = etime(e);
         if (r < T0) {
             vb = (uint32_t)(e & 3u);
-        } else if (r < T1 && r <= dur) {
+        } else if (r < T1e) {
             if (DIRECT || n_out < cap) out[n_out] = e;
             ++n_out;
         }
         lastv = (uint32_t)(e & 3u);
     };
     auto front = [&]() -> uint64_t { return rn == 1 ? rg0 : rn == 2 ? rg1 : rn == 3 ? rg2 : rg3; };
+    // emit the pending entries with time <= lim (oldest first); keeps ft
+    auto drain = [&](long long lim) {
+        while (rn > 0) {
+            const uint64_t f = front();
+            if (etime(f) > lim) {
+                ft = etime(f);
+                return;
+            }
+            emit(f);
+            --rn;
+        }
+        ft = LLONG_MAX;
+    };
     auto step = [&](long long t, uint32_t nx) {
         if (nx != xn) {
             const uint32_t E = lut[lb + nx];            // calculateSignals
@@ -114,13 +132,16 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
                     rg0 = rg1; rg1 = rg2; rg2 = rg3;
                     --rn;
                 }
+                if (rn == 0) ft = LLONG_MAX;
                 const uint32_t tv = rn > 0 ? (uint32_t)(rg0 & 3u) : lastv;
                 if (tv != E) {
                     if (rn == RD) {
                         status = 1;
+                        lim1 = 0;                       // stop at the next iteration
                     } else {
                         rg3 = rg2; rg2 = rg1; rg1 = rg0;
                         rg0 = ((uint64_t)rr << 2) | E;
+                        if (rn == 0) ft = rr;
                         ++rn;
                     }
                 }
@@ -129,13 +150,7 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
             }
             xn = nx;
         }
-        const long long lim = t + dmin;                // streaming finality
-        while (rn > 0) {
-            const uint64_t f = front();
-            if (etime(f) > lim) break;
-            emit(f);
-            --rn;
-        }
+        if (ft <= t + dmin) drain(t + dmin);           // streaming finality
     };
 
     step(s.tau0, x0);                                   // the slice's halo start
@@ -143,12 +158,13 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
     for (;;) {
         ++n_it;
         const uint64_t m = min(min(h[0], h[1]), min(h[2], h[3]));
-        if (m >= lim1 || status) break;
+        if (m >= lim1) break;
+        const uint64_t mt = m | 3ull;                  // h[i] <= mt  <=>  pin i changes at t
         const long long t = etime(m);
         uint32_t nx = xn;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            if ((h[i] ^ m) < 4ull) {                   // pin i changes at t
+            if (h[i] <= mt) {                          // pin i changes at t
                 nx = (nx & ~(3u << (2 * i))) | (norm_code((uint32_t)(h[i] & 3u)) << (2 * i));
                 ++c[i].ptr;
                 if (--c[i].rem == 0) {
@@ -156,19 +172,16 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
                     if (g.rem) { c[i].ptr = g.ptr; c[i].rem = g.rem; c[i].ck = g.ck; }
                 }
                 h[i] = c[i].rem ? *c[i].ptr : kInfEntry;
+#if GLS_PF
                 if ((((uintptr_t)c[i].ptr) & 127u) == 0 && c[i].rem > 32)
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(c[i].ptr + 32));
+#endif
             }
         }
         n_evals += (t >= T0);
         step(t, nx);
     }
-    while (rn > 0) {                                    // final for this slice below T1
-        const uint64_t f = front();
-        if (etime(f) >= T1) break;
-        emit(f);
-        --rn;
-    }
+    drain(T1 - 1);                                      // final for this slice below T1
     cnt = n_out;
     evals = n_evals;
     events = n_ev;
@@ -446,6 +459,25 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         if (lane == 0) {
             atomicAdd(&p.ctl->lane_iters, sum_it);
             atomicAdd(&p.ctl->warp_iters, 32ull * mx);
+        }
+        // balance counters: slice lanes against their group's longest lane, packed lanes, idle lanes
+        const unsigned gid = slice_lane ? (unsigned)B.u_chunk[u0] : (nun > 0 ? 1000u : 2000u);
+        const unsigned gm = __match_any_sync(FULL, gid);
+        const unsigned gmax = __reduce_max_sync(gm, its_sum);
+        const unsigned long long b0 = warp_sum64(slice_lane ? its_sum : 0u);
+        const unsigned long long b1 = warp_sum64(slice_lane ? gmax : 0u);
+        const unsigned long long b2 = warp_sum64(!slice_lane && nun > 0 ? its_sum : 0u);
+        const unsigned n_sl = __popc(__ballot_sync(FULL, slice_lane));
+        const unsigned n_pk = __popc(__ballot_sync(FULL, !slice_lane && nun > 0));
+        if (lane == 0) {
+            atomicAdd(&p.ctl->bal[0], b0);
+            atomicAdd(&p.ctl->bal[1], b1);
+            atomicAdd(&p.ctl->bal[2], b2);
+            atomicAdd(&p.ctl->bal[3], (unsigned long long)n_pk * mx);
+            atomicAdd(&p.ctl->bal[4], (unsigned long long)n_sl * mx);
+            atomicAdd(&p.ctl->bal[5], (unsigned long long)(32u - n_sl - n_pk) * mx);
+            atomicAdd(&p.ctl->bal[6], (unsigned long long)n_sl);
+            atomicAdd(&p.ctl->bal[7], (unsigned long long)n_pk);
         }
     }
     __syncwarp();

@@ -48,12 +48,14 @@ class gls_stats(ctypes.Structure):
                 ("fanin_reads", ctypes.c_int64),
                 ("lane_utilization", ctypes.c_double), ("batches", ctypes.c_int64),
                 ("batch_lanes", ctypes.c_double), ("batch_est", ctypes.c_double),
-                ("phase_cycles", ctypes.c_double * 5), ("kernel_ms", ctypes.c_double),
+                ("phase_cycles", ctypes.c_double * 5), ("balance", ctypes.c_double * 8),
+                ("kernel_ms", ctypes.c_double),
                 ("simulate_ms", ctypes.c_double)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_}
         d["phase_cycles"] = list(self.phase_cycles)
+        d["balance"] = list(self.balance)
         return d
 
 
