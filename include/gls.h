@@ -115,8 +115,9 @@ typedef struct gls_stats {
     int64_t batches;         /* slice engine: warp batches                          */
     double batch_lanes;      /* slice engine: mean lanes holding work per batch     */
     double batch_est;        /* slice engine: mean expected transitions per batch   */
-    double phase_cycles[5];  /* slice engine, summed over warps: waiting + batch assembly,
-                                slice setup, slice loops, output copy, chunk completion */
+    double phase_cycles[6];  /* slice engine, summed over warps: waiting + batch assembly,
+                                slice setup, cursor location, slice loops, output copy,
+                                chunk completion */
     double balance[8];       /* slice engine lane-balance counters (loop iterations):
                                 [0] Σ over slice lanes, [1] Σ over slice lanes of their
                                 group's longest lane, [2] Σ over packed lanes, [3] Σ over

@@ -697,7 +697,7 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
         s.batches = (int64_t)c.batches;
         s.batch_lanes = c.batches ? (double)c.batch_lanes / (double)c.batches : 0.0;
         s.batch_est = c.batches ? (double)c.batch_est / (double)c.batches : 0.0;
-        for (int q = 0; q < 5; ++q) s.phase_cycles[q] = (double)c.cyc[q];
+        for (int q = 0; q < 6; ++q) s.phase_cycles[q] = (double)c.cyc[q];
         for (int q = 0; q < 8; ++q) s.balance[q] = (double)c.bal[q];
         s.simulate_ms = ms_s;
         s.alg_bytes = -1;  // computed on demand by gls_get_stats

@@ -60,7 +60,7 @@ struct Ctl {
     unsigned long long batches;       // slice engine: warp batches
     unsigned long long batch_lanes;   // slice engine: lanes holding work, summed over batches
     unsigned long long batch_est;     // slice engine: expected transitions, summed over batches
-    unsigned long long cyc[5];        // slice engine, lane 0 clocks: wait/assemble, setup, run, output, complete
+    unsigned long long cyc[6];        // slice engine, lane 0 clocks: wait/assemble, setup, locate, sweep, output, complete
     unsigned long long bal[8];        // slice engine lane balance (gls_stats.balance)
 };
 

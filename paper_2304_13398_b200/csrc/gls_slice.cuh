@@ -55,7 +55,8 @@ template <bool DIRECT>
 __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s, const uint8_t* lut,
                                          const uint32_t* dtab, int dstride, uint64_t* out, uint32_t& cnt,
                                          uint32_t& vb, uint32_t& evals, uint32_t& events, uint32_t& iters,
-                                         uint32_t cap) {
+                                         uint32_t cap, long long& c_loc) {
+    const long long c_l0 = clock64();
     Cur c[4];
     uint64_t h[4];
     uint32_t xn = 0, x0 = 0;
@@ -78,6 +79,7 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
             x0 |= norm_code(init) << (2 * i);          // values in effect at tau
         }
     }
+    c_loc += clock64() - c_l0;
     const uint32_t lb = s.lut_base;
     const long long T0 = s.T0, T1 = s.T1, dmin = (long long)s.dmin;
     const long long T1e = min(T1, p.duration + 1);     // outputs in [T0, T1) and <= duration (R7)
@@ -391,7 +393,7 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
     const int u0 = B.lane_u0[lane], nun = B.lane_nu[lane];
     uint32_t used = 0, its_sum = 0;
     const long long c_asm = clock64();
-    long long c_setup = 0;
+    long long c_setup = 0, c_locate = 0;
     // a slice lane (one unit, of a chunk with several slices) publishes its start time to
     // the previous lane, whose slice ends there
     long long my_start = 0;
@@ -421,7 +423,7 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         uint32_t cnt = 0, vb = 2, ev = 0, evt = 0, its = 0;
         const uint32_t cap = used < (uint32_t)LCAP ? (uint32_t)LCAP - used : 0u;
         int st = run_slice<false>(p, s, lut, dtab, dstride, scr + (used < (uint32_t)LCAP ? used : 0u), cnt, vb,
-                                  ev, evt, its, cap);
+                                  ev, evt, its, cap, c_locate);
         if (st == 1) {
             // pending ring overflow: exact count by the per-lane engine (deep ring if needed)
             ChunkOut r{0, 0, 0, 2, false};
@@ -529,7 +531,8 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         uint64_t* dst = p.arena + off + B.u_pre[u];
         if (st == 2) {                                  // scratch overflow: re-run straight into place
             uint32_t c2, v2, e2, t2, i2;
-            run_slice<true>(p, s, lut, dtab, dstride, dst, c2, v2, e2, t2, i2, 0u);
+            long long c_dummy = 0;
+            run_slice<true>(p, s, lut, dtab, dstride, dst, c2, v2, e2, t2, i2, 0u, c_dummy);
             if (c2 != B.u_cnt[u]) atomicOr(&p.ctl->error, kErrBug);
         } else {                                        // ring overflow: per-lane engine in place
             ChunkOut r2{0, 0, 0, 2, false};
@@ -570,12 +573,14 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
     }
     const long long c_end = clock64();
     const unsigned long long setup_max = warp_max64((unsigned long long)c_setup);
+    const unsigned long long loc_max = warp_max64((unsigned long long)c_locate);
     if (lane == 0) {
         atomicAdd(&p.ctl->cyc[0], (unsigned long long)(c_asm - c_start));
         atomicAdd(&p.ctl->cyc[1], setup_max);
-        atomicAdd(&p.ctl->cyc[2], (unsigned long long)(c_run - c_asm) - setup_max);
-        atomicAdd(&p.ctl->cyc[3], (unsigned long long)(c_out - c_run));
-        atomicAdd(&p.ctl->cyc[4], (unsigned long long)(c_end - c_out));
+        atomicAdd(&p.ctl->cyc[2], loc_max);
+        atomicAdd(&p.ctl->cyc[3], (unsigned long long)(c_run - c_asm) - setup_max - loc_max);
+        atomicAdd(&p.ctl->cyc[4], (unsigned long long)(c_out - c_run));
+        atomicAdd(&p.ctl->cyc[5], (unsigned long long)(c_end - c_out));
     }
     return true;
 }

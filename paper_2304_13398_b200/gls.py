@@ -48,7 +48,7 @@ class gls_stats(ctypes.Structure):
                 ("fanin_reads", ctypes.c_int64),
                 ("lane_utilization", ctypes.c_double), ("batches", ctypes.c_int64),
                 ("batch_lanes", ctypes.c_double), ("batch_est", ctypes.c_double),
-                ("phase_cycles", ctypes.c_double * 5), ("balance", ctypes.c_double * 8),
+                ("phase_cycles", ctypes.c_double * 6), ("balance", ctypes.c_double * 8),
                 ("kernel_ms", ctypes.c_double),
                 ("simulate_ms", ctypes.c_double)]
 
