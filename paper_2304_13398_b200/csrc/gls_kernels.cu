@@ -697,7 +697,8 @@ __device__ void gate_complete(const SimParams& p, uint32_t gi, uint32_t base, ui
 // Whole warp: record a finished chunk (descriptor, stats); the gate's last
 // chunk completes the gate.
 template <bool DATAFLOW>
-__device__ void chunk_done(const SimParams& p, unsigned long long id, const ChunkResult& R) {
+__device__ void chunk_done(const SimParams& p, unsigned long long id, const ChunkResult& R,
+                           unsigned long long* acc = nullptr) {
     const int lane = threadIdx.x & 31;
     unsigned prev = 0;
     if (lane == 0) {
@@ -708,10 +709,17 @@ __device__ void chunk_done(const SimParams& p, unsigned long long id, const Chun
             p.ck_vb[id] = (uint8_t)R.vb;
             prev = atom_add_release(&p.gate_done[R.gi], 1u);
         }
-        atomicAdd(&p.ctl->gate_evals, R.evals);
-        atomicAdd(&p.ctl->events, R.events);
-        atomicAdd(&p.ctl->out_trans, (unsigned long long)R.total);
-        atomicAdd(&p.ctl->chunks, 1ull);
+        if (acc) {                                      // per-warp statistics (slice engine)
+            acc[0] += R.evals;
+            acc[1] += R.events;
+            acc[2] += (unsigned long long)R.total;
+            acc[3] += 1ull;
+        } else {
+            atomicAdd(&p.ctl->gate_evals, R.evals);
+            atomicAdd(&p.ctl->events, R.events);
+            atomicAdd(&p.ctl->out_trans, (unsigned long long)R.total);
+            atomicAdd(&p.ctl->chunks, 1ull);
+        }
     }
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (R.fits && prev == R.nch - 1)
@@ -788,9 +796,11 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
         for (int g = (int)gwarp; g < p.level_off[1]; g += (int)nwarps) plan_gate(p, (uint32_t)g);
         if (ENGINE == 0) {
             unsigned long long carry = ~0ull;
+            if (lane == 0) sl::acc_zero(slice_batch_smem(s_dyn));
             while (sl::slice_batch<true>(p, s_lut, reinterpret_cast<uint32_t*>(s_dyn), slice_batch_smem(s_dyn),
                                          carry, 0, 0, nullptr)) {
             }
+            if (lane == 0) sl::acc_flush(p, slice_batch_smem(s_dyn));
         } else {
         // pull published chunks until every gate is complete (Alg. 1 loop)
         for (;;) {
@@ -834,6 +844,7 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
     } else {
         unsigned gen = 0;
         unsigned long long ck_begin = (unsigned long long)p.P;
+        if (ENGINE == 0 && lane == 0) sl::acc_zero(slice_batch_smem(s_dyn));
         for (int l = 1; l <= p.L; ++l) {
             plan_level(p, l, gwarp, nwarps);
             if (grid_barrier(p.ctl, p.nblocks, gen)) return;
@@ -845,6 +856,7 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
                 while (sl::slice_batch<false>(p, s_lut, reinterpret_cast<uint32_t*>(s_dyn), slice_batch_smem(s_dyn),
                                               carry, ck_begin, ck_end - ck_begin, &p.work[l])) {
                 }
+                if (lane == 0) sl::acc_flush(p, slice_batch_smem(s_dyn));   // (before the barrier: counts are read after it)
             } else {
                 const unsigned long long n = ck_end - ck_begin;
                 for (;;) {

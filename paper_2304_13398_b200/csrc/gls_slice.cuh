@@ -18,6 +18,9 @@
 namespace gls {
 namespace sl {
 
+#ifndef GLS_DISCARD
+#define GLS_DISCARD 1
+#endif
 #ifndef GLS_PF
 #define GLS_PF 1
 #endif
@@ -203,7 +206,12 @@ constexpr int W_LANE = 128;            // a batch is filled up to 32 x W_LANE ex
 constexpr int W_MIN = 32;              // fewest expected transitions per lane (slice setup cost)
 constexpr int MAXC = 96;               // chunks per batch
 constexpr int MAXU = 160;              // units per batch
+// per-warp statistics, accumulated in shared memory and added to Ctl once when the
+// warp runs out of work (instead of ~25 same-address atomics per batch)
+enum Acc { A_EVALS, A_EVENTS, A_OUTS, A_CHUNKS, A_LANE_IT, A_WARP_IT, A_BATCHES, A_BLANES, A_BEST, A_CYC, A_BAL = A_CYC + 6,
+           A_N = A_BAL + 8 };
 struct Batch {
+    unsigned long long acc[A_N];
     unsigned long long id[MAXC];
     uint8_t nsl[MAXC];                     // slices of the chunk
     uint8_t first_unit[MAXC];
@@ -253,6 +261,21 @@ __device__ __forceinline__ void fill_dtab(uint32_t* dtab, int dstride, const Chu
         dtab[(i * 6 + 4) * dstride] = d.y;
         dtab[(i * 6 + 5) * dstride] = min(d.x, d.y);
     }
+}
+
+// lane 0: zero / flush this warp's statistics
+__device__ __forceinline__ void acc_zero(Batch& B) {
+    for (int k = 0; k < A_N; ++k) B.acc[k] = 0;
+}
+__device__ void acc_flush(const SimParams& p, Batch& B) {
+    unsigned long long* const dst[A_N] = {
+        &p.ctl->gate_evals, &p.ctl->events, &p.ctl->out_trans, &p.ctl->chunks, &p.ctl->lane_iters, &p.ctl->warp_iters,
+        &p.ctl->batches, &p.ctl->batch_lanes, &p.ctl->batch_est, &p.ctl->cyc[0], &p.ctl->cyc[1], &p.ctl->cyc[2],
+        &p.ctl->cyc[3], &p.ctl->cyc[4], &p.ctl->cyc[5], &p.ctl->bal[0], &p.ctl->bal[1], &p.ctl->bal[2],
+        &p.ctl->bal[3], &p.ctl->bal[4], &p.ctl->bal[5], &p.ctl->bal[6], &p.ctl->bal[7]};
+    for (int k = 0; k < A_N; ++k)
+        if (B.acc[k]) atomicAdd(dst[k], B.acc[k]);
+    acc_zero(B);
 }
 
 // Whole warp: evaluate one batch.  Returns false when there is no more work
@@ -328,8 +351,8 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
             ++nc;
         }
         if (nc > 0) {
-            atomicAdd(&p.ctl->batches, 1ull);
-            atomicAdd(&p.ctl->batch_est, total);
+            B.acc[A_BATCHES] += 1ull;
+            B.acc[A_BEST] += total;
         }
         // phase 2: spread the 32 lanes in proportion to the expected work (w per lane)
         const unsigned long long w = max((unsigned long long)W_MIN, (total + 31) / 32);
@@ -375,7 +398,7 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         if (nc > 0) {
             int busy = 0;
             for (int q = 0; q < 32; ++q) busy += B.lane_nu[q] > 0;
-            atomicAdd(&p.ctl->batch_lanes, (unsigned long long)busy);
+            B.acc[A_BLANES] += (unsigned long long)busy;
         }
         p.deep_wtop[warp_global_id()] = 0;          // this warp's deep scratch, reused per batch
     }
@@ -459,8 +482,8 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = max(mx, (unsigned long long)__shfl_xor_sync(FULL, mx, o));
         if (lane == 0) {
-            atomicAdd(&p.ctl->lane_iters, sum_it);
-            atomicAdd(&p.ctl->warp_iters, 32ull * mx);
+            B.acc[A_LANE_IT] += sum_it;
+            B.acc[A_WARP_IT] += 32ull * mx;
         }
         // balance counters: slice lanes against their group's longest lane, packed lanes, idle lanes
         const unsigned gid = slice_lane ? (unsigned)B.u_chunk[u0] : (nun > 0 ? 1000u : 2000u);
@@ -472,14 +495,14 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         const unsigned n_sl = __popc(__ballot_sync(FULL, slice_lane));
         const unsigned n_pk = __popc(__ballot_sync(FULL, !slice_lane && nun > 0));
         if (lane == 0) {
-            atomicAdd(&p.ctl->bal[0], b0);
-            atomicAdd(&p.ctl->bal[1], b1);
-            atomicAdd(&p.ctl->bal[2], b2);
-            atomicAdd(&p.ctl->bal[3], (unsigned long long)n_pk * mx);
-            atomicAdd(&p.ctl->bal[4], (unsigned long long)n_sl * mx);
-            atomicAdd(&p.ctl->bal[5], (unsigned long long)(32u - n_sl - n_pk) * mx);
-            atomicAdd(&p.ctl->bal[6], (unsigned long long)n_sl);
-            atomicAdd(&p.ctl->bal[7], (unsigned long long)n_pk);
+            B.acc[A_BAL + 0] += b0;
+            B.acc[A_BAL + 1] += b1;
+            B.acc[A_BAL + 2] += b2;
+            B.acc[A_BAL + 3] += (unsigned long long)n_pk * mx;
+            B.acc[A_BAL + 4] += (unsigned long long)n_sl * mx;
+            B.acc[A_BAL + 5] += (unsigned long long)(32u - n_sl - n_pk) * mx;
+            B.acc[A_BAL + 6] += (unsigned long long)n_sl;
+            B.acc[A_BAL + 7] += (unsigned long long)n_pk;
         }
     }
     __syncwarp();
@@ -517,6 +540,11 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         }
         for (; e < cu; ++e) dst[e] = src[e];
     }
+#if GLS_DISCARD
+    // the staged outputs are dead: drop their L2 lines without writing them back to DRAM
+    for (uint32_t q = 0; q < min(used, (uint32_t)LCAP); q += 16)
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(scr + q) : "memory");
+#endif
     // ---- units whose scratch or ring overflowed: the owning lane writes them in place
     for (int u = u0; u < u0 + nun; ++u) {
         const int st = B.u_st[u];
@@ -569,18 +597,18 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         }
         R.evals = e1;
         R.events = e2;
-        chunk_done<DATAFLOW>(p, id, R);
+        chunk_done<DATAFLOW>(p, id, R, B.acc);
     }
     const long long c_end = clock64();
     const unsigned long long setup_max = warp_max64((unsigned long long)c_setup);
     const unsigned long long loc_max = warp_max64((unsigned long long)c_locate);
     if (lane == 0) {
-        atomicAdd(&p.ctl->cyc[0], (unsigned long long)(c_asm - c_start));
-        atomicAdd(&p.ctl->cyc[1], setup_max);
-        atomicAdd(&p.ctl->cyc[2], loc_max);
-        atomicAdd(&p.ctl->cyc[3], (unsigned long long)(c_run - c_asm) - setup_max - loc_max);
-        atomicAdd(&p.ctl->cyc[4], (unsigned long long)(c_out - c_run));
-        atomicAdd(&p.ctl->cyc[5], (unsigned long long)(c_end - c_out));
+        B.acc[A_CYC + 0] += (unsigned long long)(c_asm - c_start);
+        B.acc[A_CYC + 1] += setup_max;
+        B.acc[A_CYC + 2] += loc_max;
+        B.acc[A_CYC + 3] += (unsigned long long)(c_run - c_asm) - setup_max - loc_max;
+        B.acc[A_CYC + 4] += (unsigned long long)(c_out - c_run);
+        B.acc[A_CYC + 5] += (unsigned long long)(c_end - c_out);
     }
     return true;
 }
