@@ -1,0 +1,52 @@
+"""Pins for tests/winhash.py (CPU): the vectorised window hash equals the oracle's
+own per-net hashes on the full window and a per-net loop on sub-windows."""
+import numpy as np
+
+from oracle import oracle
+from paper_2304_13398_b200 import workloads as W
+from winhash import splitmix64, window_hash
+
+
+def _loop_hash(offsets, trans, lo, hi):
+    M = (1 << 64) - 1
+
+    def sm(x):
+        x = (x + 0x9E3779B97F4A7C15) & M
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+        return x ^ (x >> 31)
+    out = []
+    for n in range(len(offsets) - 1):
+        es = [int(x) for x in trans[offsets[n]:offsets[n + 1]] if lo <= (int(x) >> 2) <= hi]
+        h = sm(0x9E3779B97F4A7C15 ^ len(es))
+        for x in es:
+            h = sm(h ^ x)
+        out.append(h)
+    return np.array(out, np.uint64)
+
+
+def _run():
+    nl = W.recipe_netlist(7, 400, 12, 40)
+    spec = W.make_stimspec(7, 40, 120, "skewed", mean_trans=30, wcv=4.0)
+    o, t = W.generate_stimuli(spec)
+    st = W.to_stimuli(o, t)
+    r = oracle.simulate(nl.num_inputs, nl.gate_type, nl.fanin_offsets, nl.fanin_net, nl.pin_delay,
+                        st.offsets, st.trans, spec.duration)
+    return r, spec
+
+
+def test_splitmix_known_value():
+    # splitmix64 of 0 (the generator's first output from state 0, a published constant)
+    with np.errstate(over="ignore"):
+        assert int(splitmix64(np.array([0], np.uint64))[0]) == 0xE220A8397B1DCDAF
+
+
+def test_full_window_equals_oracle_hashes():
+    r, spec = _run()
+    assert np.array_equal(window_hash(r.offsets, r.trans, 0, spec.duration), r.hashes)
+
+
+def test_sub_windows_equal_loop():
+    r, spec = _run()
+    for lo, hi in [(0, 0), (10_000, 350_000), (600_000, spec.duration), (spec.duration + 1, spec.duration + 5)]:
+        assert np.array_equal(window_hash(r.offsets, r.trans, lo, hi), _loop_hash(r.offsets, r.trans, lo, hi))
