@@ -176,27 +176,6 @@ def run_reference(a):
     return 0
 
 
-def window_hash_numpy(offsets, trans, t_lo, t_hi):
-    """Per-net hash of transitions with t_lo <= t <= t_hi, from a CSR."""
-    M = (1 << 64) - 1
-
-    def sm(x):
-        x = (x + 0x9E3779B97F4A7C15) & M
-        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
-        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
-        return x ^ (x >> 31)
-    out = np.zeros(len(offsets) - 1, np.uint64)
-    for n in range(len(offsets) - 1):
-        e = trans[offsets[n]:offsets[n + 1]]
-        t = (e >> np.uint64(2)).astype(np.int64)
-        e = e[(t >= t_lo) & (t <= t_hi)]
-        h = sm(0x9E3779B97F4A7C15 ^ len(e))
-        for x in e:
-            h = sm(h ^ int(x))
-        out[n] = h
-    return out
-
-
 def balance_str(s):
     """slice-engine lane balance: (within slice groups, slice lanes vs batch max, packed vs batch max, idle share)"""
     b = s.get("balance") or [0] * 8

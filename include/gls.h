@@ -200,14 +200,15 @@ int gls_simulate(gls_ctx *ctx, int64_t duration);
  * HOST pointers.  GLS_ESTATE if no successful simulation. */
 int gls_get_waveforms(gls_ctx *ctx, int64_t *offsets, uint64_t *transitions,
                       int64_t capacity, int64_t *total_out);
-/* Per-net 64-bit hash, host array [num_inputs + num_gates], net order:
- * h = splitmix64(0x9E3779B97F4A7C15 ^ n); h = splitmix64(h ^ e) for each of the
- * net's n packed entries e.  Computed on the device. */
+/* Per-net 64-bit results checksum, host array [num_inputs + num_gates], net order:
+ * h = splitmix64(0x9E3779B97F4A7C15 ^ n) XOR (XOR over j = 0..n-1 of
+ * splitmix64(e_j + (j + 1) * 0xD1B54A32D192ED03)), e_j the net's j-th packed entry
+ * (order-sensitive, computed warp-parallel on the device). */
 int gls_get_net_hashes(gls_ctx *ctx, uint64_t *hashes);
 /* Same into a DEVICE array (for NCCL gathers). */
 int gls_get_net_hashes_device(gls_ctx *ctx, uint64_t *d_hashes);
-/* Same hash over only the transitions with t_lo <= t <= t_hi (host array, net
- * order).  Used to verify time windows (multi-GPU sharding, sampled parity at
+/* Same checksum over only the transitions with t_lo <= t <= t_hi, j counted from
+ * the first of them (host array, net order).  Used to verify time windows (multi-GPU sharding, sampled parity at
  * full size).  GLS_EINVAL if t_hi < t_lo. */
 int gls_get_net_hashes_window(gls_ctx *ctx, int64_t t_lo, int64_t t_hi, uint64_t *hashes);
 /* Per-net transition counts, host int64 [num_inputs + num_gates]. */

@@ -370,14 +370,18 @@ void oracle_get(const oracle_result_t *r, int64_t *offsets, uint64_t *trans)
     offsets[(int64_t)r->P + r->G] = o;
 }
 
-/* Per-net 64-bit hash: h = splitmix64(C ^ len), then h = splitmix64(h ^ e)
- * for each packed entry e. */
+/* Per-net 64-bit results checksum (not part of the method):
+ * h = splitmix64(C ^ n) XOR the XOR over positions j = 0..n-1 of
+ * splitmix64(e_j + (j + 1) * K), e_j the j-th packed entry (t << 2 | v),
+ * C = 0x9E3779B97F4A7C15, K = 0xD1B54A32D192ED03, arithmetic mod 2^64. */
 void oracle_hashes(const oracle_result_t *r, uint64_t *h)
 {
     for (int64_t i = 0; i < (int64_t)r->P + r->G; i++) {
         uint64_t x = splitmix64(0x9E3779B97F4A7C15ull ^ (uint64_t)r->w[i].n);
-        for (int64_t j = 0; j < r->w[i].n; j++)
-            x = splitmix64(x ^ (((uint64_t)r->w[i].t[j] << 2) | r->w[i].v[j]));
+        for (int64_t j = 0; j < r->w[i].n; j++) {
+            const uint64_t e = ((uint64_t)r->w[i].t[j] << 2) | r->w[i].v[j];
+            x ^= splitmix64(e + (uint64_t)(j + 1) * 0xD1B54A32D192ED03ull);
+        }
         h[i] = x;
     }
 }

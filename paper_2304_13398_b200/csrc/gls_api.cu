@@ -109,6 +109,7 @@ struct DevBuf {
         p = nullptr;
         n = 0;
     }
+    cudaError_t ensure(size_t count) { return n >= count && p ? cudaSuccess : alloc(count); }
     ~DevBuf() { release(); }
 };
 
@@ -156,6 +157,7 @@ struct gls_ctx {
     DevBuf<uint8_t> d_ck_vb;
     DevBuf<uint64_t> d_deep;
     DevBuf<uint64_t> d_wscr;
+    DevBuf<uint64_t> d_hash;                // result checksums (kept: no malloc/free per readback)
     DevBuf<Ctl> d_ctl;
     DevBuf<unsigned> d_flag;
     DevBuf<unsigned long long> d_flag64;
@@ -806,12 +808,11 @@ int gls_get_net_hashes_window(gls_ctx* ctx, int64_t t_lo, int64_t t_hi, uint64_t
     if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
     if (t_hi < t_lo) return fail(ctx, GLS_EINVAL, "t_hi < t_lo");
     const int64_t N = (int64_t)ctx->P + ctx->G;
-    DevBuf<uint64_t> d;
-    CK(d.alloc(N));
     cudaSetDevice(ctx->device);
-    CK(launch_hashes_window(params(ctx), ctx->d_perm.p, t_lo, t_hi, d.p, ctx->stream));
+    CK(ctx->d_hash.ensure(N));
+    CK(launch_hashes_window(params(ctx), ctx->d_perm.p, t_lo, t_hi, ctx->d_hash.p, ctx->stream));
+    if (N) CK(cudaMemcpyAsync(hashes, ctx->d_hash.p, sizeof(uint64_t) * N, cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
-    if (N) CK(cudaMemcpy(hashes, d.p, sizeof(uint64_t) * N, cudaMemcpyDeviceToHost));
     return GLS_OK;
 }
 
@@ -819,11 +820,12 @@ int gls_get_net_hashes(gls_ctx* ctx, uint64_t* hashes) {
     if (!ctx || !hashes) return GLS_EINVAL;
     if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
     const int64_t N = (int64_t)ctx->P + ctx->G;
-    DevBuf<uint64_t> d;
-    CK(d.alloc(N));
-    int rc = gls_get_net_hashes_device(ctx, d.p);
+    cudaSetDevice(ctx->device);
+    CK(ctx->d_hash.ensure(N));
+    int rc = gls_get_net_hashes_device(ctx, ctx->d_hash.p);
     if (rc) return rc;
-    if (N) CK(cudaMemcpy(hashes, d.p, sizeof(uint64_t) * N, cudaMemcpyDeviceToHost));
+    if (N) CK(cudaMemcpyAsync(hashes, ctx->d_hash.p, sizeof(uint64_t) * N, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return GLS_OK;
 }
 

@@ -156,6 +156,24 @@ __device__ long long time_at(const SimParams& p, uint32_t net, unsigned long lon
     return etime(p.arena[__ldcg(&p.ck_off[j]) + (idx - __ldcg(&p.ck_cum[j]))]);
 }
 
+// number of transitions of `net` with t < T (chunk start times, then inside the segment)
+__device__ unsigned long long count_before(const SimParams& p, uint32_t net, long long T) {
+    const uint32_t cb = __ldcg(&p.net_ck[net]), n = __ldcg(&p.net_nck[net]);
+    uint32_t lo = 0, hi = n;  // largest j with ck_T[j] <= T (default 0)
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldcg(&p.ck_T[cb + mid]) <= T) lo = mid; else hi = mid;
+    }
+    const uint32_t j = cb + lo;
+    const uint64_t* seg = p.arena + __ldcg(&p.ck_off[j]);
+    uint32_t a = 0, b = __ldcg(&p.ck_cnt[j]);
+    while (a < b) {
+        const uint32_t m = (a + b) >> 1;
+        if (etime(seg[m]) < T) a = m + 1; else b = m;
+    }
+    return __ldcg(&p.ck_cum[j]) + a;
+}
+
 // Cursor over one fan-in net's transitions (across its chunk segments).
 struct Cursor {
     const uint64_t* ptr;
@@ -895,23 +913,35 @@ __global__ void init_given_kernel(SimParams p, const long long* in_off) {
     }
 }
 
-// validation of device-resident given waveforms (same rules as the host path)
+// validation of device-resident given waveforms (same rules as the host path):
+// one warp per net, each lane checks consecutive pairs (coalesced): strictly
+// increasing times < 2^61, every transition changes the value, the first one
+// is not X (R6: every net starts at X).
 __global__ void validate_kernel(int32_t P, const long long* off, const uint64_t* tr, long long total,
                                 unsigned* err, unsigned long long* maxt) {
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
-        long long a = off[i], b = off[i + 1];
-        if (a < 0 || b < a || b > total) { atomicOr(err, 1u); continue; }
-        uint32_t prev = 2;
-        long long pt = -1;
-        for (long long j = a; j < b; ++j) {
-            uint64_t e = tr[j];
-            long long t = (long long)(e >> 2);
-            uint32_t v = (uint32_t)(e & 3u);
-            if (t <= pt || v == prev || t >= (1ll << 61)) { atomicOr(err, 2u); break; }
-            prev = v;
-            pt = t;
+    const int lane = threadIdx.x & 31;
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int i = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < P; i += nw) {
+        const long long a = off[i], b = off[i + 1];
+        if (a < 0 || b < a || b > total) {
+            if (lane == 0) atomicOr(err, 1u);
+            continue;
         }
-        if (pt >= 0) atomicMax(maxt, (unsigned long long)pt);
+        bool bad = false;
+        for (long long j = a + lane; j < b; j += 32) {
+            const uint64_t e = tr[j];
+            const long long t = (long long)(e >> 2);
+            const uint32_t v = (uint32_t)(e & 3u);
+            uint64_t pe = 2;                            // the value before the first transition: X
+            long long pt = -1;
+            if (j > a) {
+                pe = tr[j - 1];
+                pt = (long long)(pe >> 2);
+            }
+            bad |= t <= pt || v == (uint32_t)(pe & 3u) || t >= (1ll << 61);
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 2u);
+        if (lane == 0 && b > a) atomicMax(maxt, (unsigned long long)(tr[b - 1] >> 2));
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && off[0] != 0) atomicOr(err, 1u);
 }
@@ -923,44 +953,55 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
-// per-net hash, written in user net order
+// Per-net results checksum, written in user net order: one warp per
+// net, coalesced loads of its chunk segments, position-keyed terms XOR-reduced.
+constexpr uint64_t kHashC = 0x9E3779B97F4A7C15ull, kHashK = 0xD1B54A32D192ED03ull;
 __global__ void hash_kernel(SimParams p, const uint32_t* perm, uint64_t* out) {
     const int N = p.P + p.G;
-    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-        uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
-        uint64_t h = splitmix64(0x9E3779B97F4A7C15ull ^ (uint64_t)p.net_len[n]);
+    const int lane = threadIdx.x & 31;
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int n = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); n < N; n += nw) {
+        const uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
+        uint64_t h = 0, pos = 0;                       // pos: index of the chunk's first entry
         for (uint32_t j = cb; j < cb + nck; ++j) {
             const uint64_t* s = p.arena + p.ck_off[j];
-            uint32_t c = p.ck_cnt[j];
-            for (uint32_t q = 0; q < c; ++q) h = splitmix64(h ^ s[q]);
+            const uint32_t c = p.ck_cnt[j];
+            for (uint32_t q = lane; q < c; q += 32) h ^= splitmix64(s[q] + (pos + q + 1) * kHashK);
+            pos += c;
         }
-        int user = n < p.P ? n : p.P + (int)perm[n - p.P];
-        out[user] = h;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+        if (lane == 0) {
+            const int user = n < p.P ? n : p.P + (int)perm[n - p.P];
+            out[user] = h ^ splitmix64(kHashC ^ (uint64_t)p.net_len[n]);
+        }
     }
 }
 
-// per-net hash of the transitions with t_lo <= t <= t_hi (same definition)
+// Same checksum over the transitions with t_lo <= t <= t_hi (contiguous in each net:
+// positions counted from the first of them, found with count_before).
 __global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long t_lo, long long t_hi, uint64_t* out) {
     const int N = p.P + p.G;
-    for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < N; n += gridDim.x * blockDim.x) {
-        uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
-        unsigned long long cnt = 0;
-        for (int pass = 0; pass < 2; ++pass) {
-            uint64_t h = splitmix64(0x9E3779B97F4A7C15ull ^ (uint64_t)cnt);
-            for (uint32_t j = cb; j < cb + nck; ++j) {
-                const uint64_t* s = p.arena + p.ck_off[j];
-                uint32_t c = p.ck_cnt[j];
-                if (c == 0 || etime(s[0]) > t_hi || etime(s[c - 1]) < t_lo) continue;
-                for (uint32_t q = 0; q < c; ++q) {
-                    long long t = etime(s[q]);
-                    if (t < t_lo || t > t_hi) continue;
-                    if (pass == 0) ++cnt; else h = splitmix64(h ^ s[q]);
-                }
-            }
-            if (pass == 1) {
-                int user = n < p.P ? n : p.P + (int)perm[n - p.P];
-                out[user] = h;
-            }
+    const int lane = threadIdx.x & 31;
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int n = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); n < N; n += nw) {
+        const uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
+        const unsigned long long i0 = count_before(p, (uint32_t)n, t_lo);
+        const unsigned long long i1 = t_hi == LLONG_MAX ? (unsigned long long)p.net_len[n]
+                                                         : count_before(p, (uint32_t)n, t_hi + 1);
+        uint64_t h = 0;
+        for (uint32_t j = cb; j < cb + nck && i1 > i0; ++j) {
+            const unsigned long long c0 = p.ck_cum[j], c = p.ck_cnt[j];
+            if (c0 + c <= i0 || c0 >= i1) continue;    // chunk outside the window
+            const uint64_t* s = p.arena + p.ck_off[j];
+            const unsigned long long qa = i0 > c0 ? i0 - c0 : 0ull, qb = min(c, i1 - c0);
+            for (unsigned long long q = qa + lane; q < qb; q += 32) h ^= splitmix64(s[q] + (c0 + q - i0 + 1) * kHashK);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+        if (lane == 0) {
+            const int user = n < p.P ? n : p.P + (int)perm[n - p.P];
+            out[user] = h ^ splitmix64(kHashC ^ (uint64_t)(i1 > i0 ? i1 - i0 : 0ull));
         }
     }
 }
@@ -1008,9 +1049,9 @@ cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaS
 
 cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
                                    unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s) {
-    int blocks = (P + 255) / 256;
+    int blocks = (P + 7) / 8;                          // one warp per net
     if (blocks < 1) blocks = 1;
-    if (blocks > 4096) blocks = 4096;
+    if (blocks > 148 * 16) blocks = 148 * 16;
     validate_kernel<<<blocks, 256, 0, s>>>(P, off, tr, total, d_err, d_maxt);
     return cudaGetLastError();
 }
@@ -1018,8 +1059,8 @@ cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64
 cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s) {
     int N = p.P + p.G;
     if (N == 0) return cudaSuccess;
-    int blocks = (N + 255) / 256;
-    if (blocks > 8192) blocks = 8192;
+    int blocks = (N + 7) / 8;                          // one warp per net
+    if (blocks > 148 * 16) blocks = 148 * 16;
     hash_kernel<<<blocks, 256, 0, s>>>(p, perm, out);
     return cudaGetLastError();
 }
@@ -1028,8 +1069,8 @@ cudaError_t launch_hashes_window(const SimParams& p, const uint32_t* perm, long 
                                  uint64_t* out, cudaStream_t s) {
     int N = p.P + p.G;
     if (N == 0) return cudaSuccess;
-    int blocks = (N + 255) / 256;
-    if (blocks > 8192) blocks = 8192;
+    int blocks = (N + 7) / 8;                          // one warp per net
+    if (blocks > 148 * 16) blocks = 148 * 16;
     hash_window_kernel<<<blocks, 256, 0, s>>>(p, perm, t_lo, t_hi, out);
     return cudaGetLastError();
 }

@@ -213,6 +213,27 @@ def test_error_codes(ctx):
         with pytest.raises(gls.GlsError) as e:
             ctx.gls_set_input_waveforms(2, st.offsets, st.trans)
         assert e.value.code == gls.GLS_EINVAL
+    # violations deep inside long waveforms (another lane / loop trip of the validator),
+    # through the host and the device path
+    good = [(10 * (j + 1), j % 2) for j in range(200)]
+    for pos, kind in [(77, "time"), (150, "value"), (33, "time"), (199, "value")]:
+        w = list(good)
+        if kind == "time":
+            w[pos] = (w[pos - 1][0], w[pos][1])
+        else:
+            w[pos] = (w[pos][0], w[pos - 1][1])
+            w[pos + 1:] = [(t, 1 - v) for t, v in w[pos + 1:]]
+        st = W.stimuli_from_lists([good, w])
+        with pytest.raises(gls.GlsError) as e:
+            ctx.gls_set_input_waveforms(2, st.offsets, st.trans)
+        assert e.value.code == gls.GLS_EINVAL, (pos, kind)
+        d_off = torch.as_tensor(st.offsets, device="cuda")
+        d_tr = torch.as_tensor(st.trans.astype(np.int64), device="cuda")
+        with pytest.raises(gls.GlsError) as e:
+            ctx.gls_set_input_waveforms_device(2, d_off.data_ptr(), d_tr.data_ptr(), st.total)
+        assert e.value.code == gls.GLS_EINVAL, (pos, kind)
+    st = W.stimuli_from_lists([good, good[:150]])
+    ctx.gls_set_input_waveforms(2, st.offsets, st.trans)           # valid long waveforms pass
     st = W.stimuli_from_lists([[(50, 1)], []])
     ctx.gls_set_input_waveforms(2, st.offsets, st.trans)
     with pytest.raises(gls.GlsError) as e:

@@ -33,8 +33,8 @@ def window_hash(offsets, trans, lo, hi):
         t = (e >> np.uint64(2)).astype(np.int64)
         e = e[(t >= lo) & (t <= hi)]
         h = sm(0x9E3779B97F4A7C15 ^ len(e))
-        for x in e:
-            h = sm(h ^ int(x))
+        for j, x in enumerate(e):
+            h ^= sm((int(x) + (j + 1) * 0xD1B54A32D192ED03) & M)
         out.append(h)
     return np.array(out, dtype=np.uint64)
 

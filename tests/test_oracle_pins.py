@@ -267,8 +267,8 @@ def test_pi_verbatim_and_hash():
     for n in range(nl.num_nets):
         e = r.trans[r.offsets[n]:r.offsets[n + 1]]
         h = sm(0x9E3779B97F4A7C15 ^ len(e))
-        for x in e:
-            h = sm(h ^ int(x))
+        for j, x in enumerate(e):
+            h ^= sm((int(x) + (j + 1) * 0xD1B54A32D192ED03) & M)
         assert h == int(r.hashes[n])
 
 

@@ -19,8 +19,8 @@ def _loop_hash(offsets, trans, lo, hi):
     for n in range(len(offsets) - 1):
         es = [int(x) for x in trans[offsets[n]:offsets[n + 1]] if lo <= (int(x) >> 2) <= hi]
         h = sm(0x9E3779B97F4A7C15 ^ len(es))
-        for x in es:
-            h = sm(h ^ x)
+        for j, x in enumerate(es):
+            h ^= sm((x + (j + 1) * 0xD1B54A32D192ED03) & M)
         out.append(h)
     return np.array(out, np.uint64)
 

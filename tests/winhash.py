@@ -1,10 +1,11 @@
-"""Per-net window hash (DESIGN.md §5 definition, restricted to lo <= t <= hi) of a
+"""Per-net window checksum (DESIGN.md §5 definition, restricted to lo <= t <= hi) of a
 waveform CSR, vectorised over nets with numpy — the host side of the full-size
 parity checks.  Test infrastructure; pinned against the oracle's own per-net
 hashes and a per-net loop by tests/test_winhash.py."""
 import numpy as np
 
 _C = np.uint64(0x9E3779B97F4A7C15)
+_K = np.uint64(0xD1B54A32D192ED03)
 
 
 def splitmix64(x):
@@ -15,8 +16,9 @@ def splitmix64(x):
 
 
 def window_hash(offsets, trans, lo, hi):
-    """h = splitmix64(C ^ n), then h = splitmix64(h ^ e) over the net's n entries e with
-    lo <= time(e) <= hi, in order — for every net at once (one numpy pass per rank)."""
+    """h = splitmix64(C ^ n) XOR (XOR over j of splitmix64(e_j + (j + 1) * K)) over the net's n
+    entries e_j with lo <= time(e_j) <= hi, j their position inside the window — for every
+    net at once."""
     offsets = np.asarray(offsets, np.int64)
     trans = np.asarray(trans).view(np.uint64)
     n = len(offsets) - 1
@@ -31,11 +33,8 @@ def window_hash(offsets, trans, lo, hi):
             return h
         start = np.zeros(n, np.int64)
         start[1:] = np.cumsum(cnt)[:-1]
-        rank = np.arange(e.size, dtype=np.int64) - start[net]   # position inside the net's window
-        order = np.argsort(rank, kind="stable")
-        bounds = np.searchsorted(rank[order], np.arange(int(rank.max()) + 2))
-        for j in range(len(bounds) - 1):
-            idx = order[bounds[j]:bounds[j + 1]]
-            nn = net[idx]                                       # distinct nets
-            h[nn] = splitmix64(h[nn] ^ e[idx])
+        pos = (np.arange(e.size, dtype=np.int64) - start[net] + 1).astype(np.uint64)
+        term = splitmix64(e + pos * _K)
+        nz = np.flatnonzero(cnt)
+        h[nz] ^= np.bitwise_xor.reduceat(term, start[nz])
     return h
