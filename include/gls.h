@@ -191,6 +191,20 @@ int gls_set_input_waveforms_device(gls_ctx *ctx, int32_t num_inputs, const int64
  * bytes needed; retry after gls_set_config), GLS_ECUDA.  Synchronous: returns
  * when the result is on the device. */
 int gls_simulate(gls_ctx *ctx, int64_t duration);
+/* One time window of the same run (time-window sharding; DESIGN.md §4,
+ * reading R17): the outputs are exact on [t_begin, t_end) ∩ [0, duration] — the same
+ * transitions gls_simulate(duration) produces there — at the cost of the window plus a
+ * halo H = gls_get_halo().  From the given waveforms set last, the library keeps
+ * every transition with t_begin - H < t < t_end and collapses the earlier ones into one
+ * transition at t_begin - H carrying the value then in effect (none if X); inputs at
+ * or after t_end cannot change outputs before t_end.  It then simulates to
+ * min(duration, t_end - 1).  The result (gls_get_waveforms, hashes, stats) is that run's:
+ * transitions before t_begin may differ from the full run's (halo), the stats include
+ * the halo's work.  The full given waveforms stay in the context (a device copy), so
+ * windows can be simulated in any order, and a later gls_simulate runs the full
+ * inputs again.  Errors: as gls_simulate, and GLS_EINVAL if t_end < t_begin or
+ * t_begin < 0. */
+int gls_simulate_window(gls_ctx *ctx, int64_t t_begin, int64_t t_end, int64_t duration);
 
 /* ---- results (a10) ------------------------------------------------------ */
 /* Canonical CSR of all num_inputs + num_gates nets, in net order (given nets

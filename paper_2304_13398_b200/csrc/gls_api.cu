@@ -147,6 +147,12 @@ struct gls_ctx {
     int64_t in_total = 0;
     int64_t max_in_time = -1;
     DevBuf<long long> d_in_off;
+    // time window (gls_simulate_window): the window's slice of the given waveforms sits
+    // after them in the arena, with its own offsets; the full inputs stay in place
+    bool window_active = false;
+    int64_t prefix_total = 0;          // arena entries to keep (given waveforms [+ window slice])
+    int64_t win_max_time = -1;
+    DevBuf<long long> d_win_off;
     DevBuf<uint64_t> d_arena;
     bool arena_auto = true;
 
@@ -286,8 +292,8 @@ int ensure_arena(gls_ctx* ctx, int64_t min_entries, bool grow_max) {
         return fail(ctx, GLS_ENOMEM, "arena allocation of %lld bytes failed: %s", (long long)want * 8,
                     cudaGetErrorString(e));
     }
-    if (ctx->d_arena.p && ctx->has_inputs && ctx->in_total > 0) {
-        e = cudaMemcpyAsync(np, ctx->d_arena.p, (size_t)ctx->in_total * 8, cudaMemcpyDeviceToDevice,
+    if (ctx->d_arena.p && ctx->has_inputs && ctx->prefix_total > 0) {
+        e = cudaMemcpyAsync(np, ctx->d_arena.p, (size_t)ctx->prefix_total * 8, cudaMemcpyDeviceToDevice,
                             ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
         if (e != cudaSuccess) {
@@ -545,7 +551,9 @@ static int set_inputs_common(gls_ctx* ctx, int32_t P, int64_t total) {
 static int upload_and_validate(gls_ctx* ctx, int32_t P, const int64_t* off, const uint64_t* tr, int64_t total,
                                cudaMemcpyKind kind) {
     ctx->has_inputs = ctx->has_result = false;
+    ctx->window_active = false;
     ctx->in_total = total;
+    ctx->prefix_total = 0;                 // nothing to keep while the new inputs are uploaded
     int rc = ensure_arena(ctx, total + 1, false);
     if (rc) return rc;
     CK(ctx->d_in_off.alloc(P + 1));
@@ -567,6 +575,7 @@ static int upload_and_validate(gls_ctx* ctx, int32_t P, const int64_t* off, cons
                     (err & 2u) ? "times not strictly increasing / value repeats the previous one (first X) / time >= 2^61 " : "",
                     last_off != total ? "offsets[P] != total" : "");
     ctx->max_in_time = total ? (int64_t)mt : -1;
+    ctx->prefix_total = total;
     ctx->has_inputs = true;
     return GLS_OK;
 }
@@ -595,14 +604,65 @@ int gls_set_input_waveforms_device(gls_ctx* ctx, int32_t P, const int64_t* d_off
     return upload_and_validate(ctx, P, d_off, d_tr, total, cudaMemcpyDeviceToDevice);
 }
 
-int gls_simulate(gls_ctx* ctx, int64_t duration) {
-    if (!ctx) return GLS_EINVAL;
+static int simulate_run(gls_ctx* ctx, int64_t duration);
+
+static int check_run(gls_ctx* ctx, int64_t duration) {
     if (!ctx->has_netlist) return fail(ctx, GLS_ESTATE, "gls_simulate before gls_load_netlist");
     if (!ctx->has_inputs) return fail(ctx, GLS_ESTATE, "gls_simulate before gls_set_input_waveforms");
     if (duration < 0 || duration >= (1ll << 61)) return fail(ctx, GLS_ERANGE, "duration out of range");
     if (ctx->max_in_time > duration)
         return fail(ctx, GLS_ERANGE, "a given transition at %lld ps is later than the duration %lld ps",
                     (long long)ctx->max_in_time, (long long)duration);
+    return GLS_OK;
+}
+
+int gls_simulate(gls_ctx* ctx, int64_t duration) {
+    if (!ctx) return GLS_EINVAL;
+    int rc = check_run(ctx, duration);
+    if (rc) return rc;
+    ctx->window_active = false;                        // the full given waveforms
+    ctx->prefix_total = ctx->in_total;
+    return simulate_run(ctx, duration);
+}
+
+int gls_simulate_window(gls_ctx* ctx, int64_t t_begin, int64_t t_end, int64_t duration) {
+    if (!ctx) return GLS_EINVAL;
+    int rc = check_run(ctx, duration);
+    if (rc) return rc;
+    if (t_begin < 0 || t_end < t_begin) return fail(ctx, GLS_EINVAL, "window [%lld, %lld) invalid",
+                                                    (long long)t_begin, (long long)t_end);
+    cudaSetDevice(ctx->device);
+    ctx->has_result = false;
+    ctx->window_active = false;
+    ctx->prefix_total = ctx->in_total;
+    const int32_t P = ctx->P;
+    const long long t_clamp = t_begin - ctx->halo;     // reading R17
+    // per-net slice sizes -> offsets (after the full inputs, 128-byte aligned)
+    DevBuf<long long> d_cnt;
+    CK(d_cnt.alloc((size_t)P + 1));
+    CK(launch_window_count(P, ctx->d_in_off.p, ctx->d_arena.p, t_clamp, t_end, d_cnt.p, ctx->stream));
+    std::vector<long long> cnt((size_t)P + 1, 0), off((size_t)P + 1, 0);
+    if (P) CK(cudaMemcpyAsync(cnt.data(), d_cnt.p, sizeof(long long) * P, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const long long base = (ctx->in_total + 15) & ~15ll;
+    off[0] = base;
+    for (int32_t i = 0; i < P; ++i) off[i + 1] = off[i] + cnt[i];
+    const int64_t total_w = off[P] - base;
+    rc = ensure_arena(ctx, base + total_w + 1, false);  // keeps the full inputs
+    if (rc) return rc;
+    CK(ctx->d_win_off.ensure((size_t)P + 1));
+    CK(cudaMemcpyAsync(ctx->d_win_off.p, off.data(), sizeof(long long) * (P + 1), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(launch_window_fill(P, ctx->d_in_off.p, ctx->d_arena.p, t_clamp, t_end, ctx->d_win_off.p, ctx->d_arena.p,
+                          ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->window_active = true;
+    ctx->prefix_total = base + total_w;
+    const int64_t sim = std::max<int64_t>(0, std::min<int64_t>(duration, t_end - 1));
+    return simulate_run(ctx, sim);
+}
+
+static int simulate_run(gls_ctx* ctx, int64_t duration) {
     cudaSetDevice(ctx->device);
     ctx->has_result = false;
     ctx->duration = duration;
@@ -625,7 +685,7 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
         Ctl init{};
         init.chunk_top = (unsigned long long)ctx->P;
         init.work_head = (unsigned long long)ctx->P;
-        init.arena_top = (unsigned long long)((ctx->in_total + 15) & ~15ll);   // 128-byte segments
+        init.arena_top = (unsigned long long)((ctx->prefix_total + 15) & ~15ll);   // 128-byte segments
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         CK(cudaMemcpyAsync(ctx->d_ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemsetAsync(ctx->d_work.p, 0, sizeof(unsigned long long) * (ctx->L + 1), ctx->stream));
@@ -638,7 +698,7 @@ int gls_simulate(gls_ctx* ctx, int64_t duration) {
                                      : ctx->d_ck_gate.n;
             CK(cudaMemsetAsync(ctx->d_ck_gate.p, 0xff, sizeof(uint32_t) * clear, ctx->stream));
         }
-        CK(launch_init_given(p, ctx->d_in_off.p, ctx->stream));
+        CK(launch_init_given(p, ctx->window_active ? ctx->d_win_off.p : ctx->d_in_off.p, ctx->stream));
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (ctx->G > 0) CK(launch_simulate(p, blocks, ctx->stream));
         CK(cudaEventRecord(ctx->ev[2], ctx->stream));

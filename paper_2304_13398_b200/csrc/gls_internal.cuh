@@ -108,6 +108,12 @@ cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaS
 cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s);
 size_t warp_scratch_entries(int blocks);
 int max_coresident_blocks(int device, int engine, int sched, int* per_sm);
+// time-window slice of the given waveforms (gls_simulate_window): per net the number of
+// kept entries, then the entries (collapse at t_clamp, keep t_clamp < t < t_end)
+cudaError_t launch_window_count(int32_t P, const long long* off, const uint64_t* tr, long long t_clamp,
+                                long long t_end, long long* cnt, cudaStream_t s);
+cudaError_t launch_window_fill(int32_t P, const long long* off, const uint64_t* tr, long long t_clamp,
+                               long long t_end, const long long* new_off, uint64_t* out, cudaStream_t s);
 cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
                                    unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s);
 cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s);

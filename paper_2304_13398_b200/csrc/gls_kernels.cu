@@ -913,6 +913,63 @@ __global__ void init_given_kernel(SimParams p, const long long* in_off) {
     }
 }
 
+// ------------------------------------------------------------------ time windows
+// One net's slice for a window: [ia, ib) = the transitions with t_clamp < t < t_end;
+// the earlier ones collapse into one at t_clamp carrying the last value (kept unless X,
+// which every net starts at — reading R6/R17).
+__device__ __forceinline__ void window_range(const long long* off, const uint64_t* tr, int i, long long t_clamp,
+                                             long long t_end, long long& ia, long long& ib, int& collapse,
+                                             uint64_t& ce) {
+    const long long a = off[i], b = off[i + 1];
+    long long lo = a, hi = b;                          // first index with t > t_clamp
+    while (lo < hi) {
+        const long long m = (lo + hi) >> 1;
+        if ((long long)(tr[m] >> 2) <= t_clamp) lo = m + 1; else hi = m;
+    }
+    ia = lo;
+    hi = b;                                            // first index with t >= t_end
+    while (lo < hi) {
+        const long long m = (lo + hi) >> 1;
+        if ((long long)(tr[m] >> 2) < t_end) lo = m + 1; else hi = m;
+    }
+    ib = lo;
+    collapse = 0;
+    ce = 0;
+    if (ia > a && (tr[ia - 1] & 3u) != 2u) {
+        collapse = 1;
+        ce = ((uint64_t)t_clamp << 2) | (tr[ia - 1] & 3u);
+    }
+}
+__global__ void window_count_kernel(int32_t P, const long long* off, const uint64_t* tr, long long t_clamp,
+                                    long long t_end, long long* cnt) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < P; i += gridDim.x * blockDim.x) {
+        long long ia, ib;
+        int c;
+        uint64_t ce;
+        window_range(off, tr, i, t_clamp, t_end, ia, ib, c, ce);
+        cnt[i] = c + (ib - ia);
+    }
+}
+// one warp per net: coalesced copy of the kept range
+__global__ void window_fill_kernel(int32_t P, const long long* off, const uint64_t* tr, long long t_clamp,
+                                   long long t_end, const long long* new_off, uint64_t* out) {
+    const int lane = threadIdx.x & 31;
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int i = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < P; i += nw) {
+        long long ia = 0, ib = 0;
+        int c = 0;
+        uint64_t ce = 0;
+        if (lane == 0) window_range(off, tr, i, t_clamp, t_end, ia, ib, c, ce);
+        ia = __shfl_sync(0xffffffffu, ia, 0);
+        ib = __shfl_sync(0xffffffffu, ib, 0);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        ce = __shfl_sync(0xffffffffu, ce, 0);
+        uint64_t* dst = out + new_off[i];
+        if (lane == 0 && c) dst[0] = ce;
+        for (long long j = ia + lane; j < ib; j += 32) dst[c + (j - ia)] = tr[j];
+    }
+}
+
 // validation of device-resident given waveforms (same rules as the host path):
 // one warp per net, each lane checks consecutive pairs (coalesced): strictly
 // increasing times < 2^61, every transition changes the value, the first one
@@ -1044,6 +1101,24 @@ cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaS
     int blocks = (p.P + 255) / 256;
     if (blocks > 4096) blocks = 4096;
     init_given_kernel<<<blocks, 256, 0, s>>>(p, in_off);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_window_count(int32_t P, const long long* off, const uint64_t* tr, long long t_clamp,
+                                long long t_end, long long* cnt, cudaStream_t s) {
+    if (P == 0) return cudaSuccess;
+    int blocks = (P + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    window_count_kernel<<<blocks, 256, 0, s>>>(P, off, tr, t_clamp, t_end, cnt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_window_fill(int32_t P, const long long* off, const uint64_t* tr, long long t_clamp,
+                               long long t_end, const long long* new_off, uint64_t* out, cudaStream_t s) {
+    if (P == 0) return cudaSuccess;
+    int blocks = (P + 7) / 8;                          // one warp per net
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    window_fill_kernel<<<blocks, 256, 0, s>>>(P, off, tr, t_clamp, t_end, new_off, out);
     return cudaGetLastError();
 }
 

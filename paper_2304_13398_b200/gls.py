@@ -22,7 +22,7 @@ STATUS = {0: "GLS_OK", -1: "GLS_EINVAL", -2: "GLS_ECYCLE", -3: "GLS_ENOMEM", -4:
 
 EXPORTS = ["gls_create", "gls_destroy", "gls_last_error", "gls_version", "gls_set_config",
            "gls_load_netlist", "gls_set_input_waveforms", "gls_set_input_waveforms_device",
-           "gls_simulate", "gls_get_waveforms", "gls_get_net_hashes", "gls_get_net_hashes_device",
+           "gls_simulate", "gls_simulate_window", "gls_get_waveforms", "gls_get_net_hashes", "gls_get_net_hashes_device",
            "gls_get_net_hashes_window",
            "gls_get_net_counts", "gls_get_stats", "gls_get_halo", "gls_get_levels", "gls_lut_lookup"]
 
@@ -81,6 +81,7 @@ def load_library():
         "gls_set_input_waveforms": (ctypes.c_int, [vp, i32, vp, vp]),
         "gls_set_input_waveforms_device": (ctypes.c_int, [vp, i32, vp, vp, i64]),
         "gls_simulate": (ctypes.c_int, [vp, i64]),
+        "gls_simulate_window": (ctypes.c_int, [vp, i64, i64, i64]),
         "gls_get_waveforms": (ctypes.c_int, [vp, vp, vp, i64, p(i64)]),
         "gls_get_net_hashes": (ctypes.c_int, [vp, vp]),
         "gls_get_net_hashes_device": (ctypes.c_int, [vp, vp]),
@@ -192,6 +193,9 @@ class Context:
 
     def gls_simulate(self, duration):
         return self._check(self._lib.gls_simulate(self._h, int(duration)))
+
+    def gls_simulate_window(self, t_begin, t_end, duration):
+        return self._check(self._lib.gls_simulate_window(self._h, int(t_begin), int(t_end), int(duration)))
 
     def gls_get_waveforms(self) -> Waveforms:
         n = self.num_inputs + self.num_gates

@@ -276,3 +276,34 @@ def test_warp_engine_deep_pending_and_spills(ctx, seed):
     for eng in (0, 2):
         for sch in (0, 1):
             assert_same(ctx, nl, st, 61000, engine=eng, scheduler=sch, chunk_events=1 << 20, hashes=False)
+
+
+@pytest.mark.parametrize("engine", ENGINES[:2] + ENGINES[3:4], ids=EIDS[:2] + EIDS[3:4])
+def test_simulate_window_matches_full_run(ctx, engine):
+    """gls_simulate_window (reading R17 inside the library): on [t_begin, t_end) the
+    window run's transitions equal the full run's (oracle), for windows at the start,
+    inside, across chunk boundaries and at the end, in any order; a later plain
+    gls_simulate runs the full inputs again."""
+    from winhash import window_hash
+    for seed in range(4):
+        nl = W.recipe_netlist(70 + seed, 900, 15, 60)
+        spec = W.make_stimspec(70 + seed, 60, 400, "skewed", mean_trans=60, wcv=3.0)
+        o, t = W.generate_stimuli(spec)
+        st = W.to_stimuli(o, t)
+        dur = spec.duration
+        ref = run_oracle(nl, st, dur)
+        ctx.gls_set_config(chunk_events=64 if seed % 2 else 0, **engine)
+        ctx.load(nl)
+        ctx.gls_set_input_waveforms(nl.num_inputs, st.offsets, st.trans)
+        for t0, t1 in [(2_000_000, 2_500_000), (0, 300_000), (1_234_567, 3_000_001), (dur - 77_777, dur + 1),
+                       (1_000_000, 1_000_000)]:
+            ctx.gls_simulate_window(t0, t1, dur)
+            if t1 == t0:                                            # empty window: nothing promised
+                continue
+            got = ctx.gls_get_net_hashes_window(t0, t1 - 1)
+            assert np.array_equal(got, window_hash(ref.offsets, ref.trans, t0, t1 - 1)), (seed, t0, t1)
+        ctx.gls_simulate(dur)                                       # the full inputs again
+        assert np.array_equal(ctx.gls_get_waveforms().trans, ref.trans)
+        with pytest.raises(gls.GlsError) as e:
+            ctx.gls_simulate_window(10, 5, dur)
+        assert e.value.code == gls.GLS_EINVAL
