@@ -285,6 +285,8 @@ int ensure_arena(gls_ctx* ctx, int64_t min_entries, bool grow_max) {
     if (want < min_entries) want = min_entries;
     if ((int64_t)ctx->d_arena.n >= want && !grow_max) return GLS_OK;
     if ((int64_t)ctx->d_arena.n == want) return GLS_OK;
+    const bool keep = ctx->d_arena.p && ctx->has_inputs && ctx->prefix_total > 0;
+    if (!keep) ctx->d_arena.release();                 // nothing to copy: free before allocating
     uint64_t* np = nullptr;
     cudaError_t e = cudaMalloc(&np, (size_t)std::max<int64_t>(want, 1) * 8);
     if (e != cudaSuccess) {
@@ -292,7 +294,7 @@ int ensure_arena(gls_ctx* ctx, int64_t min_entries, bool grow_max) {
         return fail(ctx, GLS_ENOMEM, "arena allocation of %lld bytes failed: %s", (long long)want * 8,
                     cudaGetErrorString(e));
     }
-    if (ctx->d_arena.p && ctx->has_inputs && ctx->prefix_total > 0) {
+    if (keep) {
         e = cudaMemcpyAsync(np, ctx->d_arena.p, (size_t)ctx->prefix_total * 8, cudaMemcpyDeviceToDevice,
                             ctx->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
