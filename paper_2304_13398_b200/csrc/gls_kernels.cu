@@ -794,9 +794,14 @@ namespace gls {
 constexpr int kDtabWords = 24;   // per-thread delay table words (slice engine)
 constexpr unsigned kEmpty = 0xffffffffu;
 
-// slice engine shared memory: per-thread delay tables, then one Batch per warp
+// slice engine shared memory: per-thread delay tables, one Batch per warp, then the
+// per-thread pin cursors of the 32-bit sweep ([pin][thread] columns)
 __device__ __forceinline__ sl::Batch& slice_batch_smem(unsigned char* s_dyn) {
-    return reinterpret_cast<sl::Batch*>(s_dyn + (size_t)kDtabWords * kThreads * 4)[threadIdx.x >> 5];
+    return reinterpret_cast<sl::Batch*>(s_dyn + (size_t)kDtabWords * kThreads * 2)[threadIdx.x >> 5];
+}
+__device__ __forceinline__ sl::PinSm pin_smem(unsigned char* s_dyn) {
+    return sl::PinSm{(uint32_t)__cvta_generic_to_shared(s_dyn + (size_t)kDtabWords * kThreads * 2 +
+                                                        sl::kBatchBytes * (kThreads / 32))};
 }
 
 template <int ENGINE, bool DATAFLOW>
@@ -815,8 +820,8 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
         if (ENGINE == 0) {
             unsigned long long carry = ~0ull;
             if (lane == 0) sl::acc_zero(slice_batch_smem(s_dyn));
-            while (sl::slice_batch<true>(p, s_lut, reinterpret_cast<uint32_t*>(s_dyn), slice_batch_smem(s_dyn),
-                                         carry, 0, 0, nullptr)) {
+            while (sl::slice_batch<true>(p, s_lut, reinterpret_cast<uint16_t*>(s_dyn), slice_batch_smem(s_dyn),
+                                         carry, 0, 0, nullptr, pin_smem(s_dyn))) {
             }
             if (lane == 0) sl::acc_flush(p, slice_batch_smem(s_dyn));
         } else {
@@ -871,8 +876,8 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
                 process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
             } else if (ENGINE == 0) {
                 unsigned long long carry = ~0ull;
-                while (sl::slice_batch<false>(p, s_lut, reinterpret_cast<uint32_t*>(s_dyn), slice_batch_smem(s_dyn),
-                                              carry, ck_begin, ck_end - ck_begin, &p.work[l])) {
+                while (sl::slice_batch<false>(p, s_lut, reinterpret_cast<uint16_t*>(s_dyn), slice_batch_smem(s_dyn),
+                                              carry, ck_begin, ck_end - ck_begin, &p.work[l], pin_smem(s_dyn))) {
                 }
                 if (lane == 0) sl::acc_flush(p, slice_batch_smem(s_dyn));   // (before the barrier: counts are read after it)
             } else {
@@ -1066,7 +1071,8 @@ __global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long 
 // ------------------------------------------------------------------ launchers
 static size_t dyn_smem(int engine) {
     return engine == 2 ? wv::kSmemBytes
-                       : (engine == 0 ? (size_t)kDtabWords * kThreads * 4 + sl::kBatchBytes * (kThreads / 32) : 0);
+                       : (engine == 0 ? (size_t)kDtabWords * kThreads * 2 + sl::kBatchBytes * (kThreads / 32) + sl::kPinSmBytes
+                                      : 0);
 }
 static const void* kernel_for(int engine, int sched) {
     if (engine == 1) return (const void*)sim_kernel<1, false>;

@@ -195,6 +195,12 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
     return status;
 }
 
+}  // namespace sl
+}  // namespace gls
+#include "gls_sweep.cuh"
+namespace gls {
+namespace sl {
+
 // Per-warp batch (lane 0 assembles it from the chunk queue): published chunks
 // are claimed until the batch holds about 32 x W_LANE expected transitions;
 // then the 32 lanes are spread in proportion to the expected work w = total/32:
@@ -204,8 +210,8 @@ __device__ __forceinline__ int run_slice(const SimParams& p, const ChunkSetup& s
 // consecutive lanes and a lane's units are contiguous.
 constexpr int W_LANE = 128;            // a batch is filled up to 32 x W_LANE expected transitions
 constexpr int W_MIN = 32;              // fewest expected transitions per lane (slice setup cost)
-constexpr int MAXC = 96;               // chunks per batch
-constexpr int MAXU = 160;              // units per batch
+constexpr int MAXC = 64;               // chunks per batch
+constexpr int MAXU = 96;               // units per batch
 // per-warp statistics, accumulated in shared memory and added to Ctl once when the
 // warp runs out of work (instead of ~25 same-address atomics per batch)
 enum Acc { A_EVALS, A_EVENTS, A_OUTS, A_CHUNKS, A_LANE_IT, A_WARP_IT, A_BATCHES, A_BLANES, A_BEST, A_CYC, A_BAL = A_CYC + 6,
@@ -250,16 +256,17 @@ __device__ __forceinline__ void unit_setup(const SimParams& p, unsigned long lon
         s.tau0 = t0 - (long long)s.dmax - 1;
     }
 }
-__device__ __forceinline__ void fill_dtab(uint32_t* dtab, int dstride, const ChunkSetup& s) {
+template <class T>
+__device__ __forceinline__ void fill_dtab(T* dtab, int dstride, const ChunkSetup& s) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {                       // R1: output X takes the smaller delay
         const uint4 d = s.d[i];
-        dtab[(i * 6 + 0) * dstride] = d.z;
-        dtab[(i * 6 + 1) * dstride] = d.w;
-        dtab[(i * 6 + 2) * dstride] = min(d.z, d.w);
-        dtab[(i * 6 + 3) * dstride] = d.x;
-        dtab[(i * 6 + 4) * dstride] = d.y;
-        dtab[(i * 6 + 5) * dstride] = min(d.x, d.y);
+        dtab[(i * 6 + 0) * dstride] = (T)d.z;
+        dtab[(i * 6 + 1) * dstride] = (T)d.w;
+        dtab[(i * 6 + 2) * dstride] = (T)min(d.z, d.w);
+        dtab[(i * 6 + 3) * dstride] = (T)d.x;
+        dtab[(i * 6 + 4) * dstride] = (T)d.y;
+        dtab[(i * 6 + 5) * dstride] = (T)min(d.x, d.y);
     }
 }
 
@@ -282,9 +289,9 @@ __device__ void acc_flush(const SimParams& p, Batch& B) {
 // (dataflow: every gate done or an error; levels: the level is exhausted).
 // `carry` (lane 0) holds a claimed chunk id that did not fit the last batch.
 template <bool DATAFLOW>
-__device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_dtab, Batch& B,
+__device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint16_t* s_dtab, Batch& B,
                             unsigned long long& carry, unsigned long long lvl_begin, unsigned long long lvl_n,
-                            unsigned long long* lvl_work) {
+                            unsigned long long* lvl_work, PinSm cs) {
     const int lane = threadIdx.x & 31;
     constexpr unsigned long long NONE = ~0ull;
     int nc = 0, nu = 0;
@@ -410,8 +417,10 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
 
     uint64_t* const wscr = p.wscr + (size_t)warp_global_id() * kScratchPerWarp;
     uint64_t* scr = wscr + (size_t)lane * LCAP;
-    uint32_t* dtab = s_dtab + threadIdx.x;                // [q * blockDim.x + tid]
+    uint16_t* dtab = s_dtab + threadIdx.x;                // [q * blockDim.x + tid] (gates with dmax < 2^16)
     const int dstride = (int)blockDim.x;
+    const uint32_t lut_sa = (uint32_t)__cvta_generic_to_shared(lut);
+    const uint32_t dtab_sa = (uint32_t)__cvta_generic_to_shared(dtab);
     // ---- each lane: its units, in order
     const int u0 = B.lane_u0[lane], nun = B.lane_nu[lane];
     uint32_t used = 0, its_sum = 0;
@@ -441,12 +450,26 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         unit_setup(p, B.id[j], B.u_slice[u], B.nsl[j], s, gi, nch,
                    (slice_lane && nb_same && lane < 31) ? &nb_start : nullptr);
         if (B.u_slice[u] == 0) B.c_T0[j] = s.T0;
-        fill_dtab(dtab, dstride, s);
+        if (s.dmax < kFastDelay) fill_dtab(dtab, dstride, s);
         c_setup += clock64() - c_us;
         uint32_t cnt = 0, vb = 2, ev = 0, evt = 0, its = 0;
         const uint32_t cap = used < (uint32_t)LCAP ? (uint32_t)LCAP - used : 0u;
-        int st = run_slice<false>(p, s, lut, dtab, dstride, scr + (used < (uint32_t)LCAP ? used : 0u), cnt, vb,
+        int st;
+        if (s.dmax < kFastDelay) {
+            uint32_t res[5];
+            st = run_slice32<false>(p, s, lut_sa, dtab_sa, cs, scr + (used < (uint32_t)LCAP ? used : 0u), cap,
+                                    res, &c_locate);
+            cnt = res[0];
+            vb = res[1];
+            ev = res[2];
+            evt = res[3];
+            its = res[4];
+        } else {
+            uint32_t dl[24];                                // long delays: 64-bit sweep, table in local memory
+            fill_dtab(dl, 1, s);
+            st = run_slice<false>(p, s, lut, dl, 1, scr + (used < (uint32_t)LCAP ? used : 0u), cnt, vb,
                                   ev, evt, its, cap, c_locate);
+        }
         if (st == 1) {
             // pending ring overflow: exact count by the per-lane engine (deep ring if needed)
             ChunkOut r{0, 0, 0, 2, false};
@@ -555,12 +578,20 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint32_t* s_
         ChunkSetup s;
         uint32_t gi, nch;
         unit_setup(p, B.id[j], B.u_slice[u], B.nsl[j], s, gi, nch, nullptr);
-        fill_dtab(dtab, dstride, s);
+        if (s.dmax < kFastDelay) fill_dtab(dtab, dstride, s);
         uint64_t* dst = p.arena + off + B.u_pre[u];
         if (st == 2) {                                  // scratch overflow: re-run straight into place
             uint32_t c2, v2, e2, t2, i2;
             long long c_dummy = 0;
-            run_slice<true>(p, s, lut, dtab, dstride, dst, c2, v2, e2, t2, i2, 0u, c_dummy);
+            if (s.dmax < kFastDelay) {
+                uint32_t res[5];
+                run_slice32<true>(p, s, lut_sa, dtab_sa, cs, dst, 0u, res, &c_dummy);
+                c2 = res[0];
+            } else {
+                uint32_t dl[24];
+                fill_dtab(dl, 1, s);
+                run_slice<true>(p, s, lut, dl, 1, dst, c2, v2, e2, t2, i2, 0u, c_dummy);
+            }
             if (c2 != B.u_cnt[u]) atomicOr(&p.ctl->error, kErrBug);
         } else {                                        // ring overflow: per-lane engine in place
             ChunkOut r2{0, 0, 0, 2, false};

@@ -129,6 +129,29 @@ def test_large_times(ctx, engine):
     assert_same(ctx, nl, W.stimuli_from_lists(waves), 13 * (1 << 29), **engine)
 
 
+@pytest.mark.parametrize("engine", ENGINES[:2], ids=EIDS[:2])
+@pytest.mark.parametrize("seed", range(4))
+def test_rebase_boundaries(ctx, seed, engine):
+    """Glitch-dense bursts straddling multiples of 2^29 ps: the 32-bit sweep moves its
+    time base there (gls_sweep.cuh) with schedules pending across the move."""
+    rng = np.random.Generator(np.random.PCG64(4000 + seed))
+    nl = W.random_dag(950 + seed, 4, 40, max_delay=30)
+    waves = []
+    for p in range(4):
+        ts = set()
+        for k in range(1, 9):
+            c = k * (1 << 29) + int(rng.integers(-60, 60))
+            ts.update(int(x) for x in c + rng.integers(-40, 40, size=6))
+        w, prev = [], 2
+        for t in sorted(ts):
+            v = int(rng.choice([x for x in range(4) if x != prev and not (not w and x == 2)]))
+            w.append((t, v))
+            prev = v
+        waves.append(w)
+    st = W.stimuli_from_lists(waves)
+    assert_same(ctx, nl, st, 9 * (1 << 29), chunk_events=int(rng.integers(3, 40)), **engine)
+
+
 @pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 def test_empty_and_constant_inputs(ctx, engine):
     nl = W.random_dag(902, 4, 30, max_delay=5)
