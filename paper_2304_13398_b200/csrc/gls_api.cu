@@ -207,7 +207,7 @@ int64_t free_bytes(gls_ctx* ctx) {
     return (int64_t)fr;
 }
 
-int default_M(int engine) { return engine == 0 ? 4096 : engine == 1 ? 256 : 2048; }
+int default_M(int engine) { return engine == 0 ? 16384 : engine == 1 ? 256 : 2048; }
 
 SimParams params(gls_ctx* ctx) {
     SimParams p{};

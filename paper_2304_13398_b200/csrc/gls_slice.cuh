@@ -25,7 +25,10 @@ namespace sl {
 #define GLS_PF 1
 #endif
 constexpr int RD = 4;                  // register pending ring depth
-constexpr int LCAP = 1024;             // per-lane output scratch entries
+#ifndef GLS_LCAP
+#define GLS_LCAP 2048
+#endif
+constexpr int LCAP = GLS_LCAP;            // per-lane output scratch entries
 constexpr int E_MIN = 32;              // fewest expected transitions per lane
 constexpr unsigned FULL = 0xffffffffu;
 constexpr size_t kScratchPerWarp = 32u * LCAP;
@@ -208,10 +211,17 @@ namespace sl {
 // quantiles of its longest fan-in); smaller chunks are packed whole, several
 // per lane.  Units are assigned in lane order, so the slices of a chunk sit on
 // consecutive lanes and a lane's units are contiguous.
-constexpr int W_LANE = 128;            // a batch is filled up to 32 x W_LANE expected transitions
+#ifndef GLS_WLANE
+#define GLS_WLANE 256
+#endif
+constexpr int W_LANE = GLS_WLANE;           // a batch is filled up to 32 x W_LANE expected transitions
 constexpr int W_MIN = 32;              // fewest expected transitions per lane (slice setup cost)
-constexpr int MAXC = 64;               // chunks per batch
-constexpr int MAXU = 96;               // units per batch
+#ifndef GLS_MAXC
+#define GLS_MAXC 16
+#define GLS_MAXU 48
+#endif
+constexpr int MAXC = GLS_MAXC;         // chunks per batch
+constexpr int MAXU = GLS_MAXU;         // units per batch
 // per-warp statistics, accumulated in shared memory and added to Ctl once when the
 // warp runs out of work (instead of ~25 same-address atomics per batch)
 enum Acc { A_EVALS, A_EVENTS, A_OUTS, A_CHUNKS, A_LANE_IT, A_WARP_IT, A_BATCHES, A_BLANES, A_BEST, A_CYC, A_BAL = A_CYC + 6,

@@ -1,6 +1,10 @@
 #!/bin/bash
-# A/B timing of library variants: tools/ab.sh "libA libB ..." "cfg1 cfg2 ..."
-for L in $1; do for c in $2; do
-  GLS_LIB=paper_2304_13398_b200/$L.so timeout 300 python bench.py --config $c --steps 2 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 \
-    | grep "warmup 2" | sed -E 's/, [0-9]+ gate-evals, [0-9]+ outputs, [0-9]+ chunks//' | cut -c1-260 | sed "s/^\[bench\] warmup 2:/$L $c/"
-done; done
+# A/B of library variants on the default bench workload: tools/ab.sh TAG variant...
+# (variant "default" = paper_2304_13398_b200/libgls.so, else paper_2304_13398_b200/libgls_<v>.so)
+TAG=$1; shift
+O=gpurun_out/$TAG; mkdir -p $O
+for v in "$@"; do
+  if [ "$v" = default ]; then unset GLS_LIB; else export GLS_LIB=$PWD/paper_2304_13398_b200/libgls_$v.so; fi
+  timeout 600 python bench.py --steps 2 --warmup 2 --no-cpu-baseline --no-e2e ${BENCH_ARGS:-} > $O/bench_$v.json 2> $O/bench_$v.log
+  echo "== $v"; tail -1 $O/bench_$v.log | cut -c1-330
+done
