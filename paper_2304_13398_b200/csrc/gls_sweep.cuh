@@ -148,16 +148,15 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
     int rn = 0;
     uint32_t ftq = kRelInf;                             // oldest pending entry (none: inf)
     uint32_t Eprev = 2, lastv = 2, vb = 2;
-    uint32_t n_out = 0, n_ev = 0, n_evals = 0, n_it = 0;
+    uint32_t n_out = 0, n_ev = 0, n_evals = 0;
     int status = 0;
 
-    auto emit = [&](uint32_t e) {
-        if (e < t0q) {
-            vb = e & 3u;
-        } else if (e < t1q) {
-            if (DIRECT || n_out < cap) out[n_out] = (uint64_t)e + b4;
-            ++n_out;
-        }
+    auto emit = [&](uint32_t e) {                       // a final schedule (predicated)
+        const bool before = e < t0q;
+        vb = before ? (e & 3u) : vb;
+        const bool w = !before && e < t1q;
+        if (w && (DIRECT || n_out < cap)) out[n_out] = (uint64_t)e + b4;
+        n_out += w ? 1u : 0u;
         lastv = e & 3u;
     };
     auto front = [&]() -> uint32_t { return rn == 1 ? rg0 : rn == 2 ? rg1 : rn == 3 ? rg2 : rg3; };
@@ -179,10 +178,10 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
                 uint32_t del = 0xffffffffu;
                 do {
                     const int b = __ffs(cm) - 1;
-                    const uint32_t fo = (xn >> b) & 3u, fn = (nn >> b) & 3u;
-                    // rank 0 < X < 1 on normalised codes (R2): rise iff new ranks higher
-                    const bool rise = ((fn & 1u) << 1 | (fn >> 1)) > ((fo & 1u) << 1 | (fo >> 1));
-                    del = min(del, lds16(dtab + (uint32_t)(((b >> 1) * 6 + (rise ? 3 : 0) + (int)E) * kThreads * 2)));   // min rule
+                    // rise iff rank(new) > rank(old), rank 0 < X < 1 on normalised codes (R2):
+                    // (old, new) in {(0,1), (0,X), (X,1)} = bits 1, 2, 9 of (old << 2 | new)
+                    const uint32_t rise = (0x206u >> ((((xn >> b) & 3u) << 2) | ((nn >> b) & 3u))) & 1u;
+                    del = min(del, lds16(dtab + (uint32_t)((b >> 1) * 6 + (int)rise * 3 + (int)E) * (kThreads * 2)));   // min rule
                     cm &= cm - 1;
                 } while (cm);
                 const uint32_t rq = ((tq >> 2) + del) << 2;  // appearance time, entry form
@@ -253,7 +252,6 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
             m = min(min(h0, h1), min(h2, h3));
             continue;
         }
-        ++n_it;
         const int b = h0 == m ? 0 : h1 == m ? 1 : h2 == m ? 2 : 3;
         nr = (nr & ~(3u << (2 * b))) | ((m & 3u) << (2 * b));
         // advance pin b
@@ -316,7 +314,7 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
     res[1] = vb;
     res[2] = n_evals;
     res[3] = n_ev;
-    res[4] = n_it;
+    res[4] = n_evals;
     if (!DIRECT && status == 0 && n_out > cap) status = 2;
     return status;
 }
