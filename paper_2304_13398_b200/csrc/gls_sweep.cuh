@@ -206,10 +206,14 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
                 }
                 n_ev += tq >= t0q;
                 Eprev = E;
+                // streaming finality, applied at events only: an entry with
+                // r <= t + dmin is final at t, and no event between two events can deny or
+                // reorder anything, so draining at the next event (or at the end) emits the
+                // same list in the same order
+                drain(tq + dminq);
             }
             xn = nn;
         }
-        drain(tq + dminq);                                   // streaming finality
     };
 
     int lastpin = -1;                                        // pin of the newest cp.async request
