@@ -346,7 +346,9 @@ def run_gls(a):
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "gls::sim_kernel", "kernel_ms": kms, "alg_bytes_per_launch": alg},
             "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
-            "gpu_launches": 2 * a.steps,
+            # per step: init_given_kernel + sim_kernel (gls_simulate) and fanin_reads_kernel
+            # (gls_get_stats' algorithmic-bytes count, read after every step for kernel_ms)
+            "gpu_launches": 3 * a.steps,
             "clocks": ck,
         }
         print(json.dumps(line), flush=True)

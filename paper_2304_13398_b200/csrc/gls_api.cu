@@ -130,6 +130,7 @@ struct gls_ctx {
     std::vector<uint32_t> inv;         // user gate -> internal gate
     std::vector<int64_t> net_fanout;   // internal net -> pins it drives
     DevBuf<uint32_t> d_fo_off, d_fo_gate, d_pend0, d_pend;
+    DevBuf<uint32_t> d_fanout;              // internal net -> pins it drives (algorithmic-bytes count)
     DevBuf<unsigned long long> d_deep_wtop;
     DevBuf<int32_t> d_level_off;
     DevBuf<GateInfo> d_gate;
@@ -531,6 +532,12 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
         CK(cudaMemcpy(ctx->d_pin_src.p, psrc.data(), sizeof(uint32_t) * E, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_pin_delay.p, pdel.data(), sizeof(uint4) * E, cudaMemcpyHostToDevice));
     }
+    {
+        std::vector<uint32_t> fo32(fanout.begin(), fanout.end());
+        CK(ctx->d_fanout.alloc(fo32.size()));
+        if (!fo32.empty())
+            CK(cudaMemcpy(ctx->d_fanout.p, fo32.data(), sizeof(uint32_t) * fo32.size(), cudaMemcpyHostToDevice));
+    }
     ctx->P = P;
     ctx->G = G;
     ctx->L = L;
@@ -775,13 +782,15 @@ int gls_get_stats(gls_ctx* ctx, gls_stats* out) {
     if (!ctx || !out) return GLS_EINVAL;
     if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
     if (ctx->stats.alg_bytes < 0) {
-        // algorithmic bytes: every fan-in waveform read once per pin
-        std::vector<unsigned long long> len((size_t)ctx->P + ctx->G);
-        if (!len.empty())
-            CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * len.size(), cudaMemcpyDeviceToHost));
-        long double reads = 0;
-        for (size_t n = 0; n < len.size(); ++n) reads += (long double)len[n] * (long double)ctx->net_fanout[n];
-        ctx->stats.alg_bytes = (int64_t)(8.0L * reads + 8.0L * (long double)ctx->stats.out_transitions +
+        // algorithmic bytes: every fan-in waveform read once per pin;
+        // sum over nets of length x fan-out, reduced on the device (no 8 B/net readback)
+        unsigned long long reads = 0;
+        const long long N = (long long)ctx->P + ctx->G;
+        CK(cudaMemsetAsync(ctx->d_flag64.p, 0, sizeof(unsigned long long), ctx->stream));
+        CK(launch_fanin_reads(ctx->d_net_len.p, ctx->d_fanout.p, N, ctx->d_flag64.p, ctx->stream));
+        CK(cudaMemcpyAsync(&reads, ctx->d_flag64.p, sizeof(reads), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->stats.alg_bytes = (int64_t)(8.0L * (long double)reads + 8.0L * (long double)ctx->stats.out_transitions +
                                          20.0L * ctx->E + 8.0L * ctx->G);
         ctx->stats.fanin_reads = (int64_t)reads;
     }

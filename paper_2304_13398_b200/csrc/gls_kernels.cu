@@ -789,7 +789,7 @@ __device__ void process_chunk_warp(const SimParams& p, unsigned long long id, co
 namespace gls {
 
 #ifndef GLS_MINB
-#define GLS_MINB 2
+#define GLS_MINB 3
 #endif
 constexpr int kDtabWords = 24;   // per-thread delay table words (slice engine)
 constexpr unsigned kEmpty = 0xffffffffu;
@@ -1068,6 +1068,16 @@ __global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long 
     }
 }
 
+// sum over nets of len x fan-out (measurement only)
+__global__ void fanin_reads_kernel(const unsigned long long* len, const uint32_t* fo, long long n,
+                                   unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc += len[i] * (unsigned long long)fo[i];
+    acc = warp_sum64(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 // ------------------------------------------------------------------ launchers
 static size_t dyn_smem(int engine) {
     return engine == 2 ? wv::kSmemBytes
@@ -1134,6 +1144,13 @@ cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64
     if (blocks < 1) blocks = 1;
     if (blocks > 148 * 16) blocks = 148 * 16;
     validate_kernel<<<blocks, 256, 0, s>>>(P, off, tr, total, d_err, d_maxt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fanin_reads(const unsigned long long* len, const uint32_t* fanout, long long n,
+                               unsigned long long* out, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    fanin_reads_kernel<<<148 * 4, 256, 0, s>>>(len, fanout, n, out);
     return cudaGetLastError();
 }
 

@@ -90,8 +90,7 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
                                         long long* c_loc) {
     const long long c_l0 = clock64();
     const int tid = threadIdx.x;
-    long long B = s.tau0;
-    uint64_t b4 = (uint64_t)B << 2;
+    uint64_t b4 = (uint64_t)s.tau0 << 2;                // the base B in entry form (B = (int64)b4 >> 2)
     uint32_t xr0 = 0, xn = 0;                           // raw values at tau0; normalised "previous" (all X)
     uint32_t h0 = kRelInf, h1 = kRelInf, h2 = kRelInf, h3 = kRelInf;
 #if !GLS_LA
@@ -132,13 +131,13 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
     const uint32_t dminq = s.dmin << 2;
     const long long T1e = min(s.T1, p.duration + 1);    // outputs in [T0, T1) and <= duration (R7)
     // per-base thresholds (entry form, relative to B)
-    uint32_t t0q, t1q, finq, lim;
+    uint32_t t0q, t1q, lim;
     bool more;
     auto thresholds = [&]() {
+        const long long B = (long long)b4 >> 2;
         const long long a0 = s.T0 - B, a1 = T1e - B, a2 = s.T1 - B;
         t0q = a0 <= 0 ? 0u : (uint32_t)(a0 << 2);                       // r >= T0  <=>  e >= t0q
         t1q = a1 < (1ll << 30) ? (uint32_t)(a1 << 2) : kRelInf;         // r < T1e  <=>  e < t1q
-        finq = a2 < (1ll << 30) ? (uint32_t)(a2 << 2) - 1u : kRelInf - 1u;   // r <= T1 - 1
         more = a2 > (1ll << 29);
         lim = more ? kRebaseQ : (uint32_t)(a2 << 2);                    // head >= lim: stop
     };
@@ -232,7 +231,7 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
             }
             const long long tmin = raw == kInfEntry ? LLONG_MAX : etime(raw);
             if (tmin >= s.T1) break;
-            const long long dB = tmin - B;                   // >= 2^29; pending entries < tmin are final
+            const long long dB = tmin - ((long long)b4 >> 2);   // >= 2^29; pending entries < tmin are final
             if (dB >= (1ll << 30)) {
                 drain(kRelInf - 1u);                         // every pending entry is < B + 2^30 <= tmin
             } else {
@@ -241,8 +240,7 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
                 rg0 -= sh; rg1 -= sh; rg2 -= sh; rg3 -= sh;
                 if (rn > 0) ftq -= sh;
             }
-            B = tmin;
-            b4 = (uint64_t)B << 2;
+            b4 = (uint64_t)tmin << 2;
             thresholds();
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -310,7 +308,10 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
         n_evals += tq >= t0q;
         step(tq, nr);
     }
-    drain(finq);                                             // final for this slice below T1
+    {                                                        // final for this slice below T1
+        const long long a2 = s.T1 - ((long long)b4 >> 2);
+        drain(a2 < (1ll << 30) ? (uint32_t)(a2 << 2) - 1u : kRelInf - 1u);
+    }
 #if GLS_LA
     cp_wait<0>();                                            // no copy may land in the next slice's cursors
 #endif

@@ -14,3 +14,6 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 3 > $O/bench_ref
 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
   --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $O/ncu_bench.log 2>&1
 tail -c 3000 $O/bench.json $O/bench_ref.json $O/smoke.log $O/pytest_gpu.log
+# one full ncu capture of the kernel on the c4_mini workload (source-level stalls)
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:sim_kernel -s 1 -c 1 -o $O/c4mini_full \
+  python bench.py --config c4_mini --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_full.log 2>&1
