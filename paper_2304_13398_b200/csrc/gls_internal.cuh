@@ -21,7 +21,10 @@ constexpr int kLutPerType = 4 + 16 + 64 + 256;       // arity 1..4, index = pack
 constexpr int kLutBytes = kLutPerType * kNumTypes;   // 3060 B, staged in shared memory
 constexpr uint64_t kInfEntry = ~0ull;                // head of an exhausted cursor
 constexpr int kRing = 32;                            // on-chip pending-schedule ring (power of 2)
-constexpr int kThreads = 256;                        // persistent-kernel CTA size
+#ifndef GLS_THREADS
+#define GLS_THREADS 256
+#endif
+constexpr int kThreads = GLS_THREADS;                       // persistent-kernel CTA size
 
 __host__ __device__ inline int lut_offset(int type, int arity) {
     // offset of (type, arity) table; arity 1 -> 0, 2 -> 4, 3 -> 20, 4 -> 84

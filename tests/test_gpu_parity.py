@@ -130,6 +130,17 @@ def test_large_times(ctx, engine):
 
 
 @pytest.mark.parametrize("engine", ENGINES[:2], ids=EIDS[:2])
+@pytest.mark.parametrize("lo,hi", [(5000, 5200), (0, 1000), (60000, 70000)])
+def test_delay_spread_paths(ctx, lo, hi, engine):
+    """Delays below 2^16 take the 32-bit sweep (u16 delay table), larger ones the 64-bit
+    sweep; both with large and small per-gate spreads."""
+    for seed in range(3):
+        nl = W.random_dag(970 + seed, 5, 60, max_delay=hi, min_delay=lo)
+        st = W.random_stimuli(seed, 5, 60, 40 * hi + 400, xz=0.2, max_gap=hi // 3 + 5)
+        assert_same(ctx, nl, st, 40 * hi + 500, chunk_events=int(7 + 5 * seed), **engine)
+
+
+@pytest.mark.parametrize("engine", ENGINES[:2], ids=EIDS[:2])
 @pytest.mark.parametrize("seed", range(4))
 def test_rebase_boundaries(ctx, seed, engine):
     """Glitch-dense bursts straddling multiples of 2^29 ps: the 32-bit sweep moves its
