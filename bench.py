@@ -271,6 +271,30 @@ def run_gls(a):
         ms, kms = float(allv[:, 0].max()), float(allv[:, 1].max())
         units, outs, alg = float(allv[:, 2].sum()), float(allv[:, 3].sum()), float(allv[:, 4].sum())
 
+    # N > 1 time windows: stitch the full-run per-net checksums from the ranks' windows
+    # (NCCL all_gather of per-net counts, then of position-keyed terms; shard.stitch_hashes),
+    # timed on the device after the timed region, max over ranks
+    stitch = None
+    if world > 1 and not replicas:
+        from paper_2304_13398_b200 import shard as _shard
+        lo, hi = plan["own"]
+        torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        stitched = _shard.gls_window_stitch(ctx, lo, hi, dev)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        st_ms = s0.elapsed_time(s1)
+        tt = torch.tensor([st_ms], dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(tt) for _ in range(world)]
+        torch.distributed.all_gather(allv, tt)
+        stitch = {"ms": float(torch.stack(allv).max()), "nets": int(stitched.numel()),
+                  "bytes_per_rank": int(16 * stitched.numel()),
+                  "what": "full-run per-net checksums from the time windows (all_gather of counts and "
+                          "position-keyed terms over NCCL)"}
+        del stitched
+
     # e2e through the public API with host buffers (pinned), every step:
     # H2D of the given waveforms, simulate, D2H of the per-net hashes
     e2e = None
@@ -345,7 +369,7 @@ def run_gls(a):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "gls::sim_kernel", "kernel_ms": kms, "alg_bytes_per_launch": alg},
-            "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "stitch": stitch,
             # per step: init_given_kernel + sim_kernel (gls_simulate) and fanin_reads_kernel
             # (gls_get_stats' algorithmic-bytes count, read after every step for kernel_ms)
             "gpu_launches": 3 * a.steps,

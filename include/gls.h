@@ -225,6 +225,23 @@ int gls_get_net_hashes_device(gls_ctx *ctx, uint64_t *d_hashes);
  * the first of them (host array, net order).  Used to verify time windows (multi-GPU sharding, sampled parity at
  * full size).  GLS_EINVAL if t_hi < t_lo. */
 int gls_get_net_hashes_window(gls_ctx *ctx, int64_t t_lo, int64_t t_hi, uint64_t *hashes);
+/* Time-window stitching (multi-GPU sharding): the pieces of the
+ * full-run checksum above contributed by this context's transitions with
+ * t_lo <= t <= t_hi.  DEVICE arrays of num_inputs + num_gates elements, net order:
+ *   d_counts[n] (out, int64)  number of such transitions;
+ *   d_terms[n]  (out, uint64, NULL = counts only)  XOR over them of
+ *               splitmix64(e_j + (d_base[n] + j + 1) * 0xD1B54A32D192ED03), j their
+ *               position inside the window and d_base[n] (in, int64, NULL = 0) the
+ *               number of the net's transitions before t_lo in the whole run;
+ *               if d_total (in, int64) is non-NULL, splitmix64(0x9E3779B97F4A7C15 ^
+ *               d_total[n]) is XORed in as well.
+ * With the windows of all ranks partitioning [0, duration], d_base = the exclusive
+ * prefix over ranks of d_counts, d_total = their sum passed by exactly one rank, the
+ * XOR over ranks of d_terms equals gls_get_net_hashes of the full run.  The arrays are
+ * written on the context's stream before return.  GLS_EINVAL if t_hi < t_lo or
+ * d_counts is NULL, GLS_ESTATE without a result. */
+int gls_get_net_hash_terms_device(gls_ctx *ctx, int64_t t_lo, int64_t t_hi, const int64_t *d_base,
+                                  const int64_t *d_total, int64_t *d_counts, uint64_t *d_terms);
 /* Per-net transition counts, host int64 [num_inputs + num_gates]. */
 int gls_get_net_counts(gls_ctx *ctx, int64_t *counts);
 /* Counters and timings of the last gls_simulate. */

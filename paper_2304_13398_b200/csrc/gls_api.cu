@@ -887,6 +887,18 @@ int gls_get_net_hashes_window(gls_ctx* ctx, int64_t t_lo, int64_t t_hi, uint64_t
     return GLS_OK;
 }
 
+int gls_get_net_hash_terms_device(gls_ctx* ctx, int64_t t_lo, int64_t t_hi, const int64_t* d_base,
+                                  const int64_t* d_total, int64_t* d_counts, uint64_t* d_terms) {
+    if (!ctx || !d_counts) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    if (t_hi < t_lo) return fail(ctx, GLS_EINVAL, "t_hi < t_lo");
+    cudaSetDevice(ctx->device);
+    CK(launch_hash_terms(params(ctx), ctx->d_perm.p, t_lo, t_hi, (const long long*)d_base,
+                         (const long long*)d_total, (long long*)d_counts, d_terms, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GLS_OK;
+}
+
 int gls_get_net_hashes(gls_ctx* ctx, uint64_t* hashes) {
     if (!ctx || !hashes) return GLS_EINVAL;
     if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");

@@ -120,6 +120,11 @@ cudaError_t launch_window_fill(int32_t P, const long long* off, const uint64_t* 
 cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64_t* tr, long long total,
                                    unsigned* d_err, unsigned long long* d_maxt, cudaStream_t s);
 cudaError_t launch_hashes(const SimParams& p, const uint32_t* perm, uint64_t* out, cudaStream_t s);
+// time-window stitching pieces (gls_get_net_hash_terms_device): per user net, count of the
+// entries with t_lo <= t <= t_hi and (terms != NULL) their checksum terms at base + j
+cudaError_t launch_hash_terms(const SimParams& p, const uint32_t* perm, long long t_lo, long long t_hi,
+                              const long long* base, const long long* total, long long* counts, uint64_t* terms,
+                              cudaStream_t s);
 // sum over nets of len[n] * fanout[n] (fan-in reads of Alg. 2, for gls_stats.alg_bytes) into *out
 cudaError_t launch_fanin_reads(const unsigned long long* len, const uint32_t* fanout, long long n,
                                unsigned long long* out, cudaStream_t s);

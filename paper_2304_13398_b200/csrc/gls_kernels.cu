@@ -1068,6 +1068,40 @@ __global__ void hash_window_kernel(SimParams p, const uint32_t* perm, long long 
     }
 }
 
+// time-window stitching pieces: one warp per net (user order out), like hash_window_kernel
+// but with the window's position keyed from base[user] and the length term optional
+__global__ void hash_terms_kernel(SimParams p, const uint32_t* perm, long long t_lo, long long t_hi,
+                                  const long long* base, const long long* total, long long* counts,
+                                  uint64_t* terms) {
+    const int N = p.P + p.G;
+    const int lane = threadIdx.x & 31;
+    const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    for (int n = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); n < N; n += nw) {
+        const int user = n < p.P ? n : p.P + (int)perm[n - p.P];
+        const unsigned long long i0 = count_before(p, (uint32_t)n, t_lo);
+        const unsigned long long i1 = t_hi == LLONG_MAX ? (unsigned long long)p.net_len[n]
+                                                         : count_before(p, (uint32_t)n, t_hi + 1);
+        const unsigned long long cnt = i1 > i0 ? i1 - i0 : 0ull;
+        if (terms) {
+            const unsigned long long b = base ? (unsigned long long)base[user] : 0ull;
+            const uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
+            uint64_t h = 0;
+            for (uint32_t j = cb; j < cb + nck && cnt; ++j) {
+                const unsigned long long c0 = p.ck_cum[j], c = p.ck_cnt[j];
+                if (c0 + c <= i0 || c0 >= i1) continue;    // chunk outside the window
+                const uint64_t* s = p.arena + p.ck_off[j];
+                const unsigned long long qa = i0 > c0 ? i0 - c0 : 0ull, qb = min(c, i1 - c0);
+                for (unsigned long long q = qa + lane; q < qb; q += 32)
+                    h ^= splitmix64(s[q] + (b + c0 + q - i0 + 1) * kHashK);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+            if (lane == 0) terms[user] = total ? h ^ splitmix64(kHashC ^ (uint64_t)total[user]) : h;
+        }
+        if (lane == 0) counts[user] = (long long)cnt;
+    }
+}
+
 // sum over nets of len x fan-out (measurement only)
 __global__ void fanin_reads_kernel(const unsigned long long* len, const uint32_t* fo, long long n,
                                    unsigned long long* out) {
@@ -1144,6 +1178,17 @@ cudaError_t launch_validate_inputs(int32_t P, const long long* off, const uint64
     if (blocks < 1) blocks = 1;
     if (blocks > 148 * 16) blocks = 148 * 16;
     validate_kernel<<<blocks, 256, 0, s>>>(P, off, tr, total, d_err, d_maxt);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hash_terms(const SimParams& p, const uint32_t* perm, long long t_lo, long long t_hi,
+                              const long long* base, const long long* total, long long* counts, uint64_t* terms,
+                              cudaStream_t s) {
+    const int N = p.P + p.G;
+    if (N == 0) return cudaSuccess;
+    int blocks = (N + 7) / 8;                          // one warp per net
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    hash_terms_kernel<<<blocks, 256, 0, s>>>(p, perm, t_lo, t_hi, base, total, counts, terms);
     return cudaGetLastError();
 }
 

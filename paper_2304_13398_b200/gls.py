@@ -23,7 +23,7 @@ STATUS = {0: "GLS_OK", -1: "GLS_EINVAL", -2: "GLS_ECYCLE", -3: "GLS_ENOMEM", -4:
 EXPORTS = ["gls_create", "gls_destroy", "gls_last_error", "gls_version", "gls_set_config",
            "gls_load_netlist", "gls_set_input_waveforms", "gls_set_input_waveforms_device",
            "gls_simulate", "gls_simulate_window", "gls_get_waveforms", "gls_get_net_hashes", "gls_get_net_hashes_device",
-           "gls_get_net_hashes_window",
+           "gls_get_net_hashes_window", "gls_get_net_hash_terms_device",
            "gls_get_net_counts", "gls_get_stats", "gls_get_halo", "gls_get_levels", "gls_lut_lookup"]
 
 
@@ -86,6 +86,7 @@ def load_library():
         "gls_get_net_hashes": (ctypes.c_int, [vp, vp]),
         "gls_get_net_hashes_device": (ctypes.c_int, [vp, vp]),
         "gls_get_net_hashes_window": (ctypes.c_int, [vp, i64, i64, vp]),
+        "gls_get_net_hash_terms_device": (ctypes.c_int, [vp, i64, i64, vp, vp, vp, vp]),
         "gls_get_net_counts": (ctypes.c_int, [vp, vp]),
         "gls_get_stats": (ctypes.c_int, [vp, p(gls_stats)]),
         "gls_get_halo": (ctypes.c_int, [vp, p(i64)]),
@@ -219,6 +220,12 @@ class Context:
 
     def gls_get_net_hashes_device(self, d_ptr):
         return self._check(self._lib.gls_get_net_hashes_device(self._h, ctypes.c_void_p(d_ptr)))
+
+    def gls_get_net_hash_terms_device(self, t_lo, t_hi, d_base, d_total, d_counts, d_terms):
+        """Device pointers (ints, 0 = NULL): window stitching pieces (include/gls.h)."""
+        vpn = lambda x: ctypes.c_void_p(x) if x else None
+        return self._check(self._lib.gls_get_net_hash_terms_device(
+            self._h, int(t_lo), int(t_hi), vpn(d_base), vpn(d_total), vpn(d_counts), vpn(d_terms)))
 
     def gls_get_net_counts(self) -> np.ndarray:
         c = np.zeros(self.num_inputs + self.num_gates, np.int64)

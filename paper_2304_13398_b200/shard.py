@@ -5,6 +5,14 @@ Time windows: rank r of N owns clock cycles [r*C/N, (r+1)*C/N) and output times
 waveforms start `lookback_cycles(H)` cycles earlier, clamped there (reading R17),
 so every net is exact on the owned window.  No exchange happens during the
 simulation; results and timings are combined afterwards with all_gather.
+
+Stitching (`stitch_hashes`): the per-net checksum of the whole run is
+an XOR of position-keyed terms plus a length term, so it splits over time windows:
+every rank counts its owned transitions per net, the counts are all-gathered (NCCL
+over NVLink on the GPU box), each rank keys its terms from the exclusive prefix of
+the counts over the ranks before it, rank 0 adds the length term, and the XOR of the
+all-gathered terms is the full-run checksum of every net — 16 bytes per net and rank
+on the wire instead of the transitions themselves.
 """
 from __future__ import annotations
 
@@ -43,3 +51,44 @@ def all_gather_rows(values, device, group=None):
     out = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
     dist.all_gather(out, t, group=group)
     return torch.stack(out).cpu()
+
+
+def stitch_hashes(counts, terms_fn, group=None):
+    """Full-run per-net checksums from per-rank windows.
+
+    counts: this rank's per-net counts of owned transitions (int64 tensor [nets]);
+    terms_fn(base, total) -> this rank's per-net terms (int64 tensor holding the uint64
+    bits), keyed from `base` (transitions of the net owned by lower ranks) and with the
+    length term of `total` XORed in when `total` is not None (rank 0 only).
+    Returns the stitched checksums (int64 tensor, uint64 bits) on every rank."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    allc = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts, group=group)
+    allc = torch.stack(allc)
+    base = allc[:rank].sum(0) if rank > 0 else torch.zeros_like(counts)
+    total = allc.sum(0) if rank == 0 else None
+    terms = terms_fn(base, total)
+    allt = [torch.empty_like(terms) for _ in range(world)]
+    dist.all_gather(allt, terms, group=group)
+    h = allt[0].clone()
+    for t in allt[1:]:
+        h.bitwise_xor_(t)
+    return h
+
+
+def gls_window_stitch(ctx, own_lo, own_hi, device, group=None):
+    """stitch_hashes for a gls context holding this rank's window run (device arrays)."""
+    n = ctx.num_inputs + ctx.num_gates
+    counts = torch.empty(n, dtype=torch.int64, device=device)
+    ctx.gls_get_net_hash_terms_device(own_lo, own_hi, 0, 0, counts.data_ptr(), 0)
+
+    def terms_fn(base, total):
+        terms = torch.empty(n, dtype=torch.int64, device=device)
+        ctx.gls_get_net_hash_terms_device(own_lo, own_hi, base.data_ptr(),
+                                          total.data_ptr() if total is not None else 0,
+                                          torch.empty(n, dtype=torch.int64, device=device).data_ptr(),
+                                          terms.data_ptr())
+        return terms
+
+    return stitch_hashes(counts, terms_fn, group)

@@ -341,3 +341,43 @@ def test_simulate_window_matches_full_run(ctx, engine):
         with pytest.raises(gls.GlsError) as e:
             ctx.gls_simulate_window(10, 5, dur)
         assert e.value.code == gls.GLS_EINVAL
+
+
+@pytest.mark.parametrize("windows", [2, 3, 5])
+def test_window_stitch_matches_full_run(ctx, windows):
+    """Time-window stitching through the device ABI (gls_get_net_hash_terms_device +
+    shard's combination): windows simulated one after the other as the ranks would,
+    counts first, then the terms keyed from the exclusive prefix of the counts, XOR =
+    the oracle's full-run per-net checksums."""
+    nl = W.recipe_netlist(91, 1200, 18, 80)
+    spec = W.make_stimspec(91, 80, 300, "skewed", mean_trans=50, wcv=3.0)
+    o, t = W.generate_stimuli(spec)
+    st = W.to_stimuli(o, t)
+    dur = spec.duration
+    ref = run_oracle(nl, st, dur)
+    ctx.gls_set_config(chunk_events=96)
+    ctx.load(nl)
+    ctx.gls_set_input_waveforms(nl.num_inputs, st.offsets, st.trans)
+    n = nl.num_nets
+    dev = torch.device("cuda", 0)
+    cuts = [dur * k // windows for k in range(windows)] + [dur + 1]
+    counts = []
+    for a, b in zip(cuts, cuts[1:]):
+        ctx.gls_simulate_window(a, b, dur)
+        c = torch.empty(n, dtype=torch.int64, device=dev)
+        ctx.gls_get_net_hash_terms_device(a, b - 1, 0, 0, c.data_ptr(), 0)
+        counts.append(c)
+    total = torch.stack(counts).sum(0)
+    base = torch.zeros(n, dtype=torch.int64, device=dev)
+    h = torch.zeros(n, dtype=torch.int64, device=dev)
+    for k, (a, b) in enumerate(zip(cuts, cuts[1:])):
+        ctx.gls_simulate_window(a, b, dur)
+        tt = torch.empty(n, dtype=torch.int64, device=dev)
+        scratch = torch.empty(n, dtype=torch.int64, device=dev)
+        ctx.gls_get_net_hash_terms_device(a, b - 1, base.data_ptr(), total.data_ptr() if k == 0 else 0,
+                                          scratch.data_ptr(), tt.data_ptr())
+        assert torch.equal(scratch, counts[k])
+        h.bitwise_xor_(tt)
+        base += counts[k]
+    assert np.array_equal(h.cpu().numpy().view(np.uint64), ref.hashes)
+    assert np.array_equal(total.cpu().numpy(), np.diff(ref.offsets))

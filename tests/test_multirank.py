@@ -1,10 +1,12 @@
-"""World-size-2 gloo test of the time-window sharding, on CPU.
+"""World-size-2 and -3 gloo tests of the time-window sharding, on CPU.
 
 Each rank simulates its window with the ORACLE (CPU) exactly as bench.py's
 ranks do with the GPU (same rank_plan, same window generator), computes the
 per-net hashes of its owned output window, and rank 0 checks them against a
 single full run restricted to each window.  This exercises the partitioning,
-halo and gather logic without a GPU.
+halo and gather logic without a GPU, and the checksum stitching
+(shard.stitch_hashes): the XOR of the ranks' position-keyed window terms equals the
+oracle's full-run per-net checksums.
 """
 import os
 import socket
@@ -14,6 +16,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+import winhash
 from oracle import oracle
 from paper_2304_13398_b200 import shard
 from paper_2304_13398_b200 import workloads as W
@@ -71,14 +74,27 @@ def _worker(rank, world, port, q):
     allh = [torch.zeros_like(ht) for _ in range(world)]
     dist.all_gather(allh, ht)
     rows = shard.all_gather_rows([float(r.gate_evals), float(lo), float(hi)], "cpu")
+    # stitch the full-run per-net checksums from the windows (shard.stitch_hashes)
+    cnt, _ = winhash.window_terms(r.offsets, r.trans, lo, hi)
+
+    def terms_fn(base, total):
+        _, tt = winhash.window_terms(r.offsets, r.trans, lo, hi, base.numpy(),
+                                     None if total is None else total.numpy())
+        return torch.as_tensor(tt.view(np.int64))
+
+    stitched = shard.stitch_hashes(torch.as_tensor(cnt), terms_fn)
     if rank == 0:
-        q.put(([x.numpy().view(np.uint64).copy() for x in allh], rows.numpy()))
+        q.put(([x.numpy().view(np.uint64).copy() for x in allh], rows.numpy(),
+               stitched.numpy().view(np.uint64).copy()))
     dist.barrier()
     dist.destroy_process_group()
 
 
-def test_time_windows_two_ranks():
-    world = 2
+import pytest
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_time_windows_ranks(world):
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
     port = s.getsockname()[1]
@@ -88,7 +104,7 @@ def test_time_windows_two_ranks():
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    got, rows = q.get(timeout=300)
+    got, rows, stitched = q.get(timeout=300)
     for p in procs:
         p.join(60)
         assert p.exitcode == 0
@@ -107,5 +123,7 @@ def test_time_windows_two_ranks():
     assert covered[0][0] == 0 and covered[-1][1] == spec.duration
     for (a, b), (c, d) in zip(covered, covered[1:]):
         assert c == b + 1
+    # the stitched checksums are the full run's (every net, whole duration)
+    assert np.array_equal(stitched, full.hashes)
     # gate-evals of the ranks cover the full run's (halo re-evaluation may add a few)
     assert rows[:, 0].sum() >= full.gate_evals

@@ -50,3 +50,28 @@ def test_sub_windows_equal_loop():
     r, spec = _run()
     for lo, hi in [(0, 0), (10_000, 350_000), (600_000, spec.duration), (spec.duration + 1, spec.duration + 5)]:
         assert np.array_equal(window_hash(r.offsets, r.trans, lo, hi), _loop_hash(r.offsets, r.trans, lo, hi))
+
+
+def test_window_terms_split_the_full_hash():
+    """The stitching pieces over windows that tile the run XOR to the oracle's own
+    full-run per-net checksums; with base 0 and total = count a single window's
+    pieces are its window hash."""
+    from winhash import window_terms
+    nl = W.recipe_netlist(5, 300, 10, 30)
+    spec = W.make_stimspec(5, 30, 80, "random")
+    o, t = W.generate_stimuli(spec)
+    st = W.to_stimuli(o, t)
+    r = oracle.simulate(nl.num_inputs, nl.gate_type, nl.fanin_offsets, nl.fanin_net, nl.pin_delay,
+                        st.offsets, st.trans, spec.duration)
+    cuts = [0, 123_456, 400_000, 400_001, spec.duration + 1]
+    cnts = [window_terms(r.offsets, r.trans, a, b - 1)[0] for a, b in zip(cuts, cuts[1:])]
+    total = np.sum(cnts, axis=0)
+    h = np.zeros_like(r.hashes)
+    base = np.zeros_like(total)
+    for k, (a, b) in enumerate(zip(cuts, cuts[1:])):
+        _, tt = window_terms(r.offsets, r.trans, a, b - 1, base, total if k == 0 else None)
+        h ^= tt
+        base = base + cnts[k]
+    assert np.array_equal(h, r.hashes)
+    c, tt = window_terms(r.offsets, r.trans, 123_456, 399_999, None, cnts[1])
+    assert np.array_equal(tt, window_hash(r.offsets, r.trans, 123_456, 399_999))

@@ -38,3 +38,28 @@ def window_hash(offsets, trans, lo, hi):
         nz = np.flatnonzero(cnt)
         h[nz] ^= np.bitwise_xor.reduceat(term, start[nz])
     return h
+
+
+def window_terms(offsets, trans, lo, hi, base=None, total=None):
+    """Per-net stitching pieces (include/gls.h gls_get_net_hash_terms_device) for the
+    entries with lo <= time <= hi: (counts, terms), terms keyed from base[n] + j and
+    with the length term of total[n] XORed in when total is given."""
+    offsets = np.asarray(offsets, np.int64)
+    trans = np.asarray(trans).view(np.uint64)
+    n = len(offsets) - 1
+    net = np.repeat(np.arange(n, dtype=np.int64), np.diff(offsets))
+    t = (trans >> np.uint64(2)).astype(np.int64)
+    keep = (t >= lo) & (t <= hi)
+    e, net = trans[keep], net[keep]
+    cnt = np.bincount(net, minlength=n).astype(np.int64)
+    base = np.zeros(n, np.int64) if base is None else np.asarray(base, np.int64)
+    with np.errstate(over="ignore"):
+        h = np.zeros(n, np.uint64) if total is None else splitmix64(_C ^ np.asarray(total).astype(np.uint64))
+        if e.size:
+            start = np.zeros(n, np.int64)
+            start[1:] = np.cumsum(cnt)[:-1]
+            pos = (np.arange(e.size, dtype=np.int64) - start[net] + base[net] + 1).astype(np.uint64)
+            term = splitmix64(e + pos * _K)
+            nz = np.flatnonzero(cnt)
+            h[nz] ^= np.bitwise_xor.reduceat(term, start[nz])
+    return cnt, h
