@@ -57,6 +57,16 @@ __device__ __forceinline__ void cp_async8(uint32_t sa, const void* g) {
 }
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+// wait_group 0 if same (the pin's request is the newest group) else wait_group 1, without a branch
+__device__ __forceinline__ void cp_wait_pin(int b, int lastpin) {
+    asm volatile("{\n .reg .pred p;\n setp.eq.s32 p, %0, %1;\n @p cp.async.wait_group 0;\n"
+                 " @!p cp.async.wait_group 1;\n}\n" ::"r"(b), "r"(lastpin) : "memory");
+}
+// request one entry (8 B, global -> shared) and commit it as a group, if `go` (predicated)
+__device__ __forceinline__ void cp_async8_if(bool go, uint32_t sa, const void* g) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %0, 0;\n @p cp.async.ca.shared.global [%1], [%2], 8;\n"
+                 " @p cp.async.commit_group;\n}\n" ::"r"((uint32_t)go), "r"(sa), "l"(g) : "memory");
+}
 
 // per-thread cursor columns in shared memory, [pin * kThreads + tid], at fixed
 // offsets from one 32-bit shared address
@@ -262,8 +272,7 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
         uint32_t rem = lds32(cs.rem(ci)) - 1u;
         // the pin's lookahead entry (requested when the current head became the head)
 #if GLS_LA
-        if (b == lastpin) cp_wait<0>();                      // requested in the previous iteration
-        else cp_wait<1>();                                   // older requests have landed
+        cp_wait_pin(b, lastpin);                             // 0 if requested in the previous iteration, else 1
         uint64_t hn = lds64(cs.hn(ci));
 #else
         uint64_t hn = b == 0 ? hn0 : b == 1 ? hn1 : b == 2 ? hn2 : hn3;
@@ -284,10 +293,8 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
         nh = rem ? to_rel(hn, b4) : kRelInf;
         // request the pin's next entry; nothing waits for it until this pin is advanced again
 #if GLS_LA
-        if (rem > 1) {
-            cp_async8(cs.hn(ci), ptr + 1);
-            lastpin = b;
-        }
+        cp_async8_if(rem > 1, cs.hn(ci), ptr + 1);
+        lastpin = rem > 1 ? b : lastpin;
 #else
         const uint64_t* la = ptr + 1;
         const bool ld = rem > 1;
