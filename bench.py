@@ -36,6 +36,7 @@ import torch  # noqa: E402
 from paper_2304_13398_b200 import workloads as W  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+C5_SETS = 64                # BASELINE configs[4]: 64 independent stimulus sets on the 1M-gate netlist
 
 # prefix of the workload the oracle runs (cycles), sized for ~10-30 s of one core
 SAMPLE_CYCLES = {"c4_10m": 3000, "c3_1m": 60, "c7552": 1999, "c5_set": 150, "c4_mini": 3000}
@@ -197,10 +198,12 @@ def run_gls(a):
         dist.init_process_group("nccl", device_id=dev)
     cfg = a.config
     nl = build_netlist(cfg, a.seed)
-    # C5 (independent stimulus sets): one set per rank, replicas; otherwise one workload
-    # split into time windows
-    replicas = cfg == "c5_set" and world > 1
-    spec = W.config_stimspec(cfg, a.seed + (rank if replicas else 0))
+    # C5 (BASELINE configs[4]): C5_SETS independent stimulus sets on one netlist, dealt
+    # round-robin to the ranks (replicas, no exchange); otherwise one workload split into
+    # time windows
+    sets = list(range(rank, C5_SETS, world)) if cfg == "c5_set" else [0]
+    replicas = cfg == "c5_set"
+    spec = W.config_stimspec(cfg, a.seed + sets[0])
     stream = torch.cuda.current_stream(dev)
     ctx = gls.Context(local, stream.cuda_stream)
     ctx.gls_set_config(chunk_events=a.chunk_events, blocks_per_sm=a.blocks_per_sm,
@@ -218,21 +221,38 @@ def run_gls(a):
     k_hi = plan["gen_cycles"][1]
     duration = plan["duration"]
     t = time.perf_counter()
-    d_off, d_tr = W.window_stimuli(spec, *plan["gen_cycles"], dev)
+    stims = []                       # this rank's given waveforms, resident in HBM: one per set
+    for k in sets:
+        sp = W.config_stimspec(cfg, a.seed + k) if replicas else spec
+        d_off, d_tr = W.window_stimuli(sp, *plan["gen_cycles"], dev)
+        stims.append((d_off, d_tr, int(d_tr.numel())))
     torch.cuda.synchronize(dev)
-    n_in = int(d_tr.numel())
+    d_off, d_tr, n_in = stims[0]
     lens = (d_off[1:] - d_off[:-1]).double()
     wcv = float(lens.std(unbiased=False) / lens.mean()) if n_in else 0.0
-    log(f"stimuli: {n_in} transitions on {spec.num_inputs} PIs, WCV {wcv:.2f} ({time.perf_counter() - t:.1f}s)")
-    ctx.gls_set_input_waveforms_device(nl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), n_in)
+    n_in_all = sum(x[2] for x in stims)
+    log(f"stimuli: {len(stims)} set(s), {n_in_all} transitions on {spec.num_inputs} PIs, WCV {wcv:.2f} "
+        f"({time.perf_counter() - t:.1f}s)")
+    if len(stims) == 1:
+        ctx.gls_set_input_waveforms_device(nl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), n_in)
 
     def step():
-        ctx.gls_simulate(duration)
+        """One pass of the hot path over the rank's batch of input: its time window, or each
+        of its stimulus sets (set the device-resident inputs, simulate).  Returns the
+        per-simulation stats of the step (kernel time, counts)."""
+        if len(stims) == 1:
+            ctx.gls_simulate(duration)
+            return [ctx.gls_get_stats()]
+        out = []
+        for o_, t_, n_ in stims:
+            ctx.gls_set_input_waveforms_device(nl.num_inputs, o_.data_ptr(), t_.data_ptr(), n_)
+            ctx.gls_simulate(duration)
+            out.append(ctx.gls_get_stats())
+        return out
 
     for i in range(a.warmup):
         t = time.perf_counter()
-        step()
-        s = ctx.gls_get_stats()
+        s = step()[0]
         log(f"warmup {i}: kernel {s['kernel_ms']:.1f} ms, {s['gate_evals']} gate-evals, "
             f"{s['out_transitions']} outputs, {s['chunks']} chunks ({s['deep_chunks']} fallback), "
             f"lane util {s['lane_utilization']:.2f}, batches {s['batches']} x {s['batch_lanes']:.1f} lanes / "
@@ -249,19 +269,19 @@ def run_gls(a):
     kernel_ms = []
     ev0.record(stream)
     for _ in range(a.steps):
-        step()
-        kernel_ms.append(ctx.gls_get_stats()["kernel_ms"])
+        st_ = step()
+        kernel_ms.extend(x["kernel_ms"] for x in st_)
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
     ck = clocks.stop()
     ms = ev0.elapsed_time(ev1) / a.steps
-    s = ctx.gls_get_stats()
-    units = s["gate_evals"]
-    outs = s["out_transitions"]
-    alg = s["alg_bytes"]
-    kms = statistics.mean(kernel_ms)
+    s = st_[-1]
+    units = sum(x["gate_evals"] for x in st_)              # per step, this rank
+    outs = sum(x["out_transitions"] for x in st_)
+    alg = statistics.mean(x["alg_bytes"] for x in st_)      # per kernel launch
+    kms = statistics.mean(kernel_ms)                        # per kernel launch
     if world > 1:
         import torch.distributed as dist
         tt = torch.tensor([ms, kms, units, outs, alg], dtype=torch.float64, device=dev)
@@ -269,7 +289,8 @@ def run_gls(a):
         dist.all_gather(allv, tt)
         allv = torch.stack(allv).cpu().numpy()
         ms, kms = float(allv[:, 0].max()), float(allv[:, 1].max())
-        units, outs, alg = float(allv[:, 2].sum()), float(allv[:, 3].sum()), float(allv[:, 4].sum())
+        units, outs = float(allv[:, 2].sum()), float(allv[:, 3].sum())
+        alg = float(allv[:, 4].mean())                      # per launch on one GPU (roofline is per GPU)
 
     # N > 1 time windows: stitch the full-run per-net checksums from the ranks' windows
     # (NCCL all_gather of per-net counts, then of position-keyed terms; shard.stitch_hashes),
@@ -299,23 +320,27 @@ def run_gls(a):
     # H2D of the given waveforms, simulate, D2H of the per-net hashes
     e2e = None
     if not a.no_e2e:
-        h_off = torch.empty(d_off.numel(), dtype=torch.int64, pin_memory=True)
-        h_tr = torch.empty(n_in, dtype=torch.int64, pin_memory=True)
-        h_off.copy_(d_off)
-        h_tr.copy_(d_tr)
-        off_np, tr_np = h_off.numpy(), h_tr.numpy().view(np.uint64)
+        e_sets = stims[:min(len(stims), 8)]     # C5: the first (up to) 8 of the rank's sets
+        pinned = []
+        for o_, t_, n_ in e_sets:
+            h_off = torch.empty(o_.numel(), dtype=torch.int64, pin_memory=True)
+            h_tr = torch.empty(n_, dtype=torch.int64, pin_memory=True)
+            h_off.copy_(o_)
+            h_tr.copy_(t_)
+            pinned.append((h_off, h_tr))
         n_e2e = max(1, min(a.steps, 3))
         torch.cuda.synchronize(dev)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(n_e2e):
-            ctx.gls_set_input_waveforms(nl.num_inputs, off_np, tr_np)
-            ctx.gls_simulate(duration)
-            hashes = ctx.gls_get_net_hashes()
+            for h_off, h_tr in pinned:
+                ctx.gls_set_input_waveforms(nl.num_inputs, h_off.numpy(), h_tr.numpy().view(np.uint64))
+                ctx.gls_simulate(duration)
+                hashes = ctx.gls_get_net_hashes()
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = e0.elapsed_time(e1) / n_e2e
-        e_units = s["gate_evals"]
+        e_units = sum(x["gate_evals"] for x in st_[:len(e_sets)])
         if world > 1:
             import torch.distributed as dist
             tt = torch.tensor([e_ms, e_units], dtype=torch.float64, device=dev)
@@ -324,10 +349,15 @@ def run_gls(a):
             allv = torch.stack(allv).cpu().numpy()
             e_ms, e_units = float(allv[:, 0].max()), float(allv[:, 1].sum())
         e2e = {"value": e_units / (e_ms / 1e3), "unit": "gate-evals/s",
-               "h2d_bytes_per_step": int(8 * (d_off.numel() + n_in)),
-               "d2h_bytes_per_step": int(8 * hashes.size), "ms_per_step": e_ms,
-               "api": "gls_set_input_waveforms(host pinned) + gls_simulate + gls_get_net_hashes"}
-        del h_off, h_tr
+               "h2d_bytes_per_step": int(sum(8 * (o_.numel() + n_) for o_, _, n_ in e_sets)),
+               "d2h_bytes_per_step": int(8 * hashes.size * len(e_sets)), "ms_per_step": e_ms,
+               "api": "gls_set_input_waveforms(host pinned) + gls_simulate + gls_get_net_hashes" +
+                      (f", first {len(e_sets)} of the rank's {len(stims)} stimulus sets" if len(stims) > 1 else "")}
+        del pinned
+
+    if len(stims) > 1:          # the parity check below is on the first set: simulate it again
+        ctx.gls_set_input_waveforms_device(nl.num_inputs, stims[0][0].data_ptr(), stims[0][1].data_ptr(), stims[0][2])
+        ctx.gls_simulate(duration)
 
     # CPU oracle on a bounded prefix of the same workload + full-size parity there
     cpu = parity = None
@@ -357,12 +387,14 @@ def run_gls(a):
         line = {
             "metric": "gate-evals/s", "value": units / (ms / 1e3), "unit": "gate-evals/s",
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong" if world > 1 and not replicas else "weak",
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": cfg, "gates": nl.num_gates, "pis": nl.num_inputs, "pins": nl.num_pins,
                        "levels": L, "duration_ps": spec.duration, "stimulus_transitions": n_in,
                        "stimulus_wcv": round(wcv, 2), "halo_ps": H,
-                       "parallelism": (f"replicas x{world} (stimulus set seed + rank)" if replicas else
+                       **({"stimulus_sets": C5_SETS, "sets_per_rank": len(stims),
+                           "stimulus_transitions_per_rank": n_in_all} if replicas else {}),
+                       "parallelism": (f"stimulus sets round-robin over {world} rank(s), no exchange" if replicas else
                                        f"time-windows x{world}" if world > 1 else "single GPU"),
                        "cache": "working set (given + computed waveforms) >> 126 MB L2; no flush needed"},
             "output_transitions_per_s": outs / (ms / 1e3),
@@ -372,7 +404,8 @@ def run_gls(a):
             "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "stitch": stitch,
             # per step: init_given_kernel + sim_kernel (gls_simulate) and fanin_reads_kernel
             # (gls_get_stats' algorithmic-bytes count, read after every step for kernel_ms)
-            "gpu_launches": 3 * a.steps,
+            # (C5: + validate_kernel of gls_set_input_waveforms_device per set)
+            "gpu_launches": a.steps * len(stims) * (3 + (1 if len(stims) > 1 else 0)),
             "clocks": ck,
         }
         print(json.dumps(line), flush=True)
