@@ -24,6 +24,12 @@ namespace sl {
 #ifndef GLS_PF
 #define GLS_PF 1
 #endif
+#ifndef GLS_MAXSLEEP
+#define GLS_MAXSLEEP 8192      // ns: longest back-off of a warp waiting for published work
+#endif
+#ifndef GLS_ADAPT
+#define GLS_ADAPT 1            // batch fill adapts to the queue depth (dataflow scheduler)
+#endif
 constexpr int RD = 4;                  // register pending ring depth
 #ifndef GLS_LCAP
 #define GLS_LCAP 2048
@@ -311,7 +317,14 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint16_t* s_
         // phase 1: claim published chunks until the batch holds about 32 x W_LANE transitions
         unsigned long long est[MAXC];
         unsigned long long total = 0;
-        while (nc < MAXC && total < 32ull * W_LANE) {
+        // shallow queue (fewer published chunks than warps): one chunk per batch, so its
+        // slices spread over all 32 lanes and the critical path through the netlist shortens
+        unsigned long long fill = 32ull * W_LANE;
+        if (DATAFLOW && GLS_ADAPT) {
+            const unsigned long long pub = ld_relaxed_u64(&p.ctl->chunk_top), head = ld_relaxed_u64(&p.ctl->work_head);
+            if (pub < head + (unsigned long long)gridDim.x * (blockDim.x >> 5)) fill = 1;
+        }
+        while (nc < MAXC && total < fill) {
             unsigned long long id;
             if (carry != NONE) {
                 id = carry;
@@ -350,7 +363,7 @@ __device__ bool slice_batch(const SimParams& p, const uint8_t* lut, uint16_t* s_
                             break;
                         }
                         __nanosleep(ns);
-                        if (ns < 8192) ns <<= 1;
+                        if (ns < GLS_MAXSLEEP) ns <<= 1;
                     }
                     if (g == 0xffffffffu) {
                         more = false;
