@@ -983,6 +983,7 @@ __global__ void validate_kernel(int32_t P, const long long* off, const uint64_t*
                                 unsigned* err, unsigned long long* maxt) {
     const int lane = threadIdx.x & 31;
     const int nw = (int)((gridDim.x * blockDim.x) >> 5);
+    unsigned long long mx = 0;
     for (int i = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5); i < P; i += nw) {
         const long long a = off[i], b = off[i + 1];
         if (a < 0 || b < a || b > total) {
@@ -1003,8 +1004,9 @@ __global__ void validate_kernel(int32_t P, const long long* off, const uint64_t*
             bad |= t <= pt || v == (uint32_t)(pe & 3u) || t >= (1ll << 61);
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 2u);
-        if (lane == 0 && b > a) atomicMax(maxt, (unsigned long long)(tr[b - 1] >> 2));
+        if (lane == 0 && b > a) mx = max(mx, (unsigned long long)(tr[b - 1] >> 2));
     }
+    if (lane == 0 && mx) atomicMax(maxt, mx);          // one same-address atomic per warp, not per net
     if (blockIdx.x == 0 && threadIdx.x == 0 && off[0] != 0) atomicOr(err, 1u);
 }
 
