@@ -85,10 +85,10 @@ def gls_window_stitch(ctx, own_lo, own_hi, device, group=None):
 
     def terms_fn(base, total):
         terms = torch.empty(n, dtype=torch.int64, device=device)
+        scratch = torch.empty(n, dtype=torch.int64, device=device)     # the counts again
         ctx.gls_get_net_hash_terms_device(own_lo, own_hi, base.data_ptr(),
                                           total.data_ptr() if total is not None else 0,
-                                          torch.empty(n, dtype=torch.int64, device=device).data_ptr(),
-                                          terms.data_ptr())
+                                          scratch.data_ptr(), terms.data_ptr())
         return terms
 
     return stitch_hashes(counts, terms_fn, group)
