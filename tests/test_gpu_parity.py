@@ -381,3 +381,33 @@ def test_window_stitch_matches_full_run(ctx, windows):
         base += counts[k]
     assert np.array_equal(h.cpu().numpy().view(np.uint64), ref.hashes)
     assert np.array_equal(total.cpu().numpy(), np.diff(ref.offsets))
+
+
+def test_window_stitch_over_nccl_single_rank(ctx):
+    """shard.gls_window_stitch end to end over a (one-rank) NCCL process group: the
+    stitched checksums of a run owning [0, duration] are the run's own."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2304_13398_b200 import shard
+    nl = W.recipe_netlist(93, 800, 12, 50)
+    spec = W.make_stimspec(93, 50, 200, "random")
+    o, t = W.generate_stimuli(spec)
+    st = W.to_stimuli(o, t)
+    ctx.gls_set_config()
+    ctx.load(nl)
+    ctx.gls_set_input_waveforms(nl.num_inputs, st.offsets, st.trans)
+    ctx.gls_simulate(spec.duration)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    try:
+        h = shard.gls_window_stitch(ctx, 0, spec.duration, dev)
+        torch.cuda.synchronize(dev)
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(h.cpu().numpy().view(np.uint64), ctx.gls_get_net_hashes())
