@@ -1030,7 +1030,14 @@ __global__ void hash_kernel(SimParams p, const uint32_t* perm, uint64_t* out) {
         for (uint32_t j = cb; j < cb + nck; ++j) {
             const uint64_t* s = p.arena + p.ck_off[j];
             const uint32_t c = p.ck_cnt[j];
-            for (uint32_t q = lane; q < c; q += 32) h ^= splitmix64(s[q] + (pos + q + 1) * kHashK);
+            uint32_t q = lane;
+            for (; q + 96 < c; q += 128) {             // 4 independent loads in flight per lane
+                const uint64_t e0 = __ldcs(s + q), e1 = __ldcs(s + q + 32), e2 = __ldcs(s + q + 64),
+                               e3 = __ldcs(s + q + 96);
+                h ^= splitmix64(e0 + (pos + q + 1) * kHashK) ^ splitmix64(e1 + (pos + q + 33) * kHashK) ^
+                     splitmix64(e2 + (pos + q + 65) * kHashK) ^ splitmix64(e3 + (pos + q + 97) * kHashK);
+            }
+            for (; q < c; q += 32) h ^= splitmix64(__ldcs(s + q) + (pos + q + 1) * kHashK);
             pos += c;
         }
 #pragma unroll

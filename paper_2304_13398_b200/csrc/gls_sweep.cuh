@@ -24,9 +24,6 @@ constexpr uint32_t kRelInf = 0xffffffffu;
 constexpr uint32_t kRebaseQ = 0x80000000u;       // entry form of t - B = 2^29
 constexpr uint32_t kFastDelay = 1u << 16;        // gates with dmax below this use the 32-bit sweep (u16 delay table)
 
-#ifndef GLS_LA
-#define GLS_LA 1                                 // lookahead: 1 = cp.async into shared memory, 0 = registers
-#endif
 
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
     uint64_t v;
@@ -50,11 +47,6 @@ __device__ __forceinline__ uint32_t lds8(uint32_t a) {
 }
 __device__ __forceinline__ void sts64(uint32_t a, uint64_t v) { asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v)); }
 __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) { asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v)); }
-// 8-byte asynchronous global -> shared copy (LDGSTS): the thread does not wait for it
-__device__ __forceinline__ void cp_async8(uint32_t sa, const void* g) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-}
 template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 // wait_group 0 if same (the pin's request is the newest group) else wait_group 1, without a branch
@@ -103,9 +95,6 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
     uint64_t b4 = (uint64_t)s.tau0 << 2;                // the base B in entry form (B = (int64)b4 >> 2)
     uint32_t xr0 = 0, xn = 0;                           // raw values at tau0; normalised "previous" (all X)
     uint32_t h0 = kRelInf, h1 = kRelInf, h2 = kRelInf, h3 = kRelInf;
-#if !GLS_LA
-    uint64_t hn0 = kInfEntry, hn1 = kInfEntry, hn2 = kInfEntry, hn3 = kInfEntry;   // lookahead entries
-#endif
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         if ((uint32_t)i < s.k) {
@@ -119,14 +108,7 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
             sts32(cs.ck(ci), cc.ck);
             const uint64_t hn = rem > 1 ? cc.ptr[1] : kInfEntry;
             const uint32_t h = rem ? to_rel(*cc.ptr, b4) : kRelInf;
-#if GLS_LA
             sts64(cs.hn(ci), hn);
-#else
-            if (i == 0) hn0 = hn;
-            if (i == 1) hn1 = hn;
-            if (i == 2) hn2 = hn;
-            if (i == 3) hn3 = hn;
-#endif
             if (i == 0) h0 = h;
             if (i == 1) h1 = h;
             if (i == 2) h2 = h;
@@ -271,12 +253,8 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
         const uint64_t* ptr = (const uint64_t*)lds64(cs.ptr(ci)) + 1;
         uint32_t rem = lds32(cs.rem(ci)) - 1u;
         // the pin's lookahead entry (requested when the current head became the head)
-#if GLS_LA
         cp_wait_pin(b, lastpin);                             // 0 if requested in the previous iteration, else 1
         uint64_t hn = lds64(cs.hn(ci));
-#else
-        uint64_t hn = b == 0 ? hn0 : b == 1 ? hn1 : b == 2 ? hn2 : hn3;
-#endif
         uint32_t nh;
         if (rem == 0) {                                      // segment end: next non-empty segment
             const uint32_t src = s.src[b];
@@ -292,17 +270,8 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
         }
         nh = rem ? to_rel(hn, b4) : kRelInf;
         // request the pin's next entry; nothing waits for it until this pin is advanced again
-#if GLS_LA
         cp_async8_if(rem > 1, cs.hn(ci), ptr + 1);
         lastpin = rem > 1 ? b : lastpin;
-#else
-        const uint64_t* la = ptr + 1;
-        const bool ld = rem > 1;
-        if (ld && b == 0) hn0 = ldg_entry(la);
-        if (ld && b == 1) hn1 = ldg_entry(la);
-        if (ld && b == 2) hn2 = ldg_entry(la);
-        if (ld && b == 3) hn3 = ldg_entry(la);
-#endif
         sts64(cs.ptr(ci), (uint64_t)ptr);
         sts32(cs.rem(ci), rem);
         h0 = b == 0 ? nh : h0;
@@ -319,9 +288,7 @@ __device__ __noinline__ int run_slice32(const SimParams& p, const ChunkSetup& s,
         const long long a2 = s.T1 - ((long long)b4 >> 2);
         drain(a2 < (1ll << 30) ? (uint32_t)(a2 << 2) - 1u : kRelInf - 1u);
     }
-#if GLS_LA
     cp_wait<0>();                                            // no copy may land in the next slice's cursors
-#endif
     res[0] = n_out;
     res[1] = vb;
     res[2] = n_evals;
