@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 PKG := paper_2304_13398_b200
 SRC := $(PKG)/csrc/gls_api.cu $(PKG)/csrc/gls_kernels.cu
-HDR := $(PKG)/csrc/gls_internal.cuh $(PKG)/csrc/gls_slice.cuh $(PKG)/csrc/gls_sweep.cuh $(PKG)/csrc/gls_warp.cuh include/gls.h
+HDR := $(PKG)/csrc/gls_internal.cuh $(PKG)/csrc/gls_lanes.cuh include/gls.h
 
 all: $(PKG)/libgls.so oracle/liboracle.so
 
@@ -25,3 +25,7 @@ clean:
 # A/B variants for performance experiments (not used by tests)
 variant-%: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -DGLS_MINB=$* -shared -o /tmp/libgls_minb$*.so $(SRC) -lcudart
+
+# named A/B variant with extra flags: make var V=name F="-DGLS_ROUND=16"
+var: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) $(F) -shared -o $(PKG)/libgls_$(V).so $(SRC) -lcudart

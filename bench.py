@@ -181,11 +181,12 @@ def run_reference(a):
 
 
 def balance_str(s):
-    """slice-engine lane balance: (within slice groups, slice lanes vs batch max, packed vs batch max, idle share)"""
+    """engine-0 counters (gls_stats.balance): static units, units split off while running,
+    re-balancing rounds, fallback units, per batch"""
     b = s.get("balance") or [0] * 8
-    f = lambda x, y: round(x / y, 3) if y else 0.0
-    return (f"[slice-in-group {f(b[0], b[1])}, slice {f(b[0], b[4])}, packed {f(b[2], b[3])}, "
-            f"idle {f(b[5], b[3] + b[4] + b[5])}, lanes sl/pk {f(b[6], b[6] + b[7])}]")
+    nb = max(1, s.get("batches") or 1)
+    return (f"[units/batch {b[0] / nb:.1f}, splits/batch {b[1] / nb:.2f}, rounds/batch {b[2] / nb:.1f}, "
+            f"fallback units {int(b[3])}]")
 
 
 def run_gls(a):

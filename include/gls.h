@@ -81,21 +81,24 @@ typedef struct gls_config {
                                 free HBM)                     */
     int64_t chunk_capacity;  /* max (gate, time-chunk) work items per run; 0 = auto */
     int32_t chunk_events;    /* target merged input events per work item (M);
-                                0 = 16384 / 256 / 2048 for engines 0 / 1 / 2      */
+                                0 = 16384 / 256 for engines 0 / 1                  */
     int32_t blocks_per_sm;   /* persistent-kernel CTAs per SM; 0 = max co-resident */
     int32_t ring_limit;      /* TESTING: cap on the on-chip pending-schedule ring
                                 (1..32) to force the deep-backtrace path; 0 = 32 */
     int32_t engine;          /* evaluation engine of a (gate, time-chunk) item:
-                                0 = lanes on balanced time slices of one chunk per warp (default),
-                                1 = one chunk per lane (reference engine for A/B),
-                                2 = warp-cooperative tiles (merge path + warp scans) */
+                                0 = a warp's lanes on time-slice units of a batch of
+                                    items, re-balanced by splitting while they run (default),
+                                1 = one item per lane (reference engine for A/B)      */
     int32_t scheduler;       /* 0 = dataflow: a gate is scheduled when its last fan-in
                                 gate completes (Alg. 1 unlock rule) (default);
                                 1 = topological levels separated by device barriers.
                                 Engine 1 always uses levels.                        */
     int64_t deep_per_warp;   /* per-warp scratch (entries) for deep backtraces and
                                 output spills; 0 = 65536, grown automatically      */
-    int32_t reserved[2];
+    int32_t readback_mib;    /* gls_get_waveforms: device staging buffer of the
+                                canonical CSR (MiB; batches of nets go through it,
+                                one D2H each); 0 = 1024                            */
+    int32_t reserved;
 } gls_config;
 
 typedef struct gls_stats {
@@ -111,19 +114,17 @@ typedef struct gls_stats {
                                 (DESIGN.md §7): 8·Σ fan-in reads + 8·outputs +
                                 20·pins + 8·gates                                  */
     int64_t fanin_reads;     /* Σ over pins of the driving net's transitions      */
-    double lane_utilization; /* slice engine: busy lane-iterations / occupied lane slots */
-    int64_t batches;         /* slice engine: warp batches                          */
-    double batch_lanes;      /* slice engine: mean lanes holding work per batch     */
-    double batch_est;        /* slice engine: mean expected transitions per batch   */
-    double phase_cycles[6];  /* slice engine, summed over warps: waiting + batch assembly,
-                                slice setup, cursor location, slice loops, output copy,
-                                chunk completion */
-    double balance[8];       /* slice engine lane-balance counters (loop iterations):
-                                [0] Σ over slice lanes, [1] Σ over slice lanes of their
-                                group's longest lane, [2] Σ over packed lanes, [3] Σ over
-                                packed lanes of the batch's longest lane, [4] Σ over slice
-                                lanes of the batch's longest lane, [5] Σ over idle lanes of
-                                the batch's longest lane, [6] slice lanes, [7] packed lanes */
+    double lane_utilization; /* engine 0: busy lane-iterations / (32 x the busiest lane's
+                                iterations), summed over re-balancing rounds          */
+    int64_t batches;         /* engine 0: warp batches                              */
+    double batch_lanes;      /* engine 0: mean lanes holding a static unit per batch */
+    double batch_est;        /* engine 0: mean expected merged entries per batch    */
+    double phase_cycles[6];  /* engine 0, lane 0 clocks summed over warps: waiting +
+                                batch assembly, static unit boundaries, sweep (rounds),
+                                fallback + allocation + output copy, chunk completion, - */
+    double balance[8];       /* engine 0 counters: [0] static units, [1] units split off
+                                while running, [2] re-balancing rounds, [3] fallback
+                                units (per-lane ring engine), [4]-[7] unused          */
     double kernel_ms;        /* CUDA-event time of the gate-evaluation kernel      */
     double simulate_ms;      /* CUDA-event time of the whole gls_simulate          */
 } gls_stats;
@@ -176,7 +177,11 @@ int gls_load_netlist(gls_ctx *ctx, int32_t num_inputs, int32_t num_gates,
  * waveform rules of §2.1 and reading R6.  A net with no transition is
  * constant X.  Errors: GLS_EINVAL, GLS_ESTATE (no netlist / num_inputs
  * mismatch), GLS_ENOMEM, GLS_ECUDA.  May be repeated (re-simulation with a new
- * stimulus set, the netlist stays loaded). */
+ * stimulus set, the netlist stays loaded).  The stimulus is checked on a device
+ * copy (a staging buffer; device inputs in place) before it replaces the given
+ * waveforms, so a rejected one leaves the previous inputs and result in place —
+ * except when the staging buffer cannot be allocated (the arena holds nearly all
+ * HBM): then a rejected HOST stimulus leaves the context without inputs. */
 int gls_set_input_waveforms(gls_ctx *ctx, int32_t num_inputs, const int64_t *offsets,
                             const uint64_t *transitions);
 /* Same, from DEVICE pointers on the context's device (validated on the device). */
@@ -214,6 +219,25 @@ int gls_simulate_window(gls_ctx *ctx, int64_t t_begin, int64_t t_end, int64_t du
  * HOST pointers.  GLS_ESTATE if no successful simulation. */
 int gls_get_waveforms(gls_ctx *ctx, int64_t *offsets, uint64_t *transitions,
                       int64_t capacity, int64_t *total_out);
+/* The same canonical CSR built on the DEVICE (a10 / GK3 on the GPU: each net's chunk
+ * segments gathered in time order, in net order), restricted to the nets
+ * [net_lo, net_hi) and to the transitions with t_lo <= t <= t_hi (the whole run:
+ * INT64_MIN, INT64_MAX).  d_offsets: DEVICE int64 [net_hi - net_lo + 1], always written
+ * (CSR offsets from 0); d_transitions: DEVICE uint64 [capacity] or NULL (size query:
+ * only d_offsets and *total_out).  Used by multi-GPU stitching (each rank's owned time
+ * window, gathered over NCCL) and by gls_get_waveforms (which runs it batch by batch
+ * of nets through a bounded staging buffer, one D2H per batch).  Errors: GLS_EINVAL
+ * (range, t_hi < t_lo, NULL offsets), GLS_ERANGE (capacity), GLS_ESTATE (no result).
+ * Synchronous. */
+int gls_get_waveforms_range_device(gls_ctx *ctx, int64_t net_lo, int64_t net_hi, int64_t t_lo,
+                                   int64_t t_hi, int64_t *d_offsets, uint64_t *d_transitions,
+                                   int64_t capacity, int64_t *total_out);
+/* Stitching helper (multi-GPU results): for i in [0, nseg) copy the
+ * segment d_src[d_src_off[i] .. d_src_off[i+1]) to d_dst + d_dst_off[i], on the
+ * context's device and stream (one warp per segment).  All DEVICE arrays, caller-owned;
+ * segments must not overlap in d_dst.  Errors: GLS_EINVAL (NULL arrays, nseg < 0). */
+int gls_scatter_segments(gls_ctx *ctx, int64_t nseg, const int64_t *d_src_off, const uint64_t *d_src,
+                         const int64_t *d_dst_off, uint64_t *d_dst);
 /* Per-net 64-bit results checksum, host array [num_inputs + num_gates], net order:
  * h = splitmix64(0x9E3779B97F4A7C15 ^ n) XOR (XOR over j = 0..n-1 of
  * splitmix64(e_j + (j + 1) * 0xD1B54A32D192ED03)), e_j the net's j-th packed entry

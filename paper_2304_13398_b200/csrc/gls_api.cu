@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -138,6 +139,7 @@ struct gls_ctx {
     DevBuf<uint4> d_pin_delay;
     DevBuf<uint8_t> d_lut;
     DevBuf<uint32_t> d_perm;
+    DevBuf<uint32_t> d_inv;                 // user gate -> internal gate (canonical readback)
     DevBuf<uint32_t> d_net_ck, d_net_nck, d_gate_done;
     DevBuf<unsigned long long> d_gate_nin;
     DevBuf<unsigned long long> d_net_len;
@@ -208,7 +210,7 @@ int64_t free_bytes(gls_ctx* ctx) {
     return (int64_t)fr;
 }
 
-int default_M(int engine) { return engine == 0 ? 16384 : engine == 1 ? 256 : 2048; }
+int default_M(int engine) { return engine == 0 ? 16384 : 256; }
 
 SimParams params(gls_ctx* ctx) {
     SimParams p{};
@@ -286,10 +288,30 @@ int ensure_arena(gls_ctx* ctx, int64_t min_entries, bool grow_max) {
     if (want < min_entries) want = min_entries;
     if ((int64_t)ctx->d_arena.n >= want && !grow_max) return GLS_OK;
     if ((int64_t)ctx->d_arena.n == want) return GLS_OK;
-    const bool keep = ctx->d_arena.p && ctx->has_inputs && ctx->prefix_total > 0;
+    bool keep = ctx->d_arena.p && ctx->has_inputs && ctx->prefix_total > 0;
     if (!keep) ctx->d_arena.release();                 // nothing to copy: free before allocating
     uint64_t* np = nullptr;
     cudaError_t e = cudaMalloc(&np, (size_t)std::max<int64_t>(want, 1) * 8);
+    if (e != cudaSuccess && keep) {
+        // the old arena (given waveforms in its prefix) leaves too little room: move the
+        // prefix through host memory, free the old arena, allocate, copy back
+        cudaGetLastError();
+        std::vector<uint64_t> host((size_t)ctx->prefix_total);
+        e = cudaMemcpy(host.data(), ctx->d_arena.p, (size_t)ctx->prefix_total * 8, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) {
+            ctx->d_arena.release();
+            keep = false;
+            e = cudaMalloc(&np, (size_t)std::max<int64_t>(want, 1) * 8);
+            if (e == cudaSuccess) e = cudaMemcpy(np, host.data(), (size_t)ctx->prefix_total * 8, cudaMemcpyHostToDevice);
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                if (np) cudaFree(np);
+                ctx->has_inputs = ctx->has_result = false;   // the given waveforms are gone with the old arena
+                return fail(ctx, GLS_ENOMEM, "arena allocation of %lld bytes failed (inputs dropped): %s",
+                            (long long)want * 8, cudaGetErrorString(e));
+            }
+        }
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(ctx, GLS_ENOMEM, "arena allocation of %lld bytes failed: %s", (long long)want * 8,
@@ -390,10 +412,11 @@ void gls_destroy(gls_ctx* ctx) {
 int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
     if (!ctx || !cfg) return GLS_EINVAL;
     if (cfg->arena_bytes < 0 || cfg->chunk_capacity < 0 || cfg->chunk_events < 0 || cfg->blocks_per_sm < 0 ||
-        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 2 ||
-        cfg->scheduler < 0 || cfg->scheduler > 1 || cfg->deep_per_warp < 0)
+        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 1 ||
+        cfg->scheduler < 0 || cfg->scheduler > 1 || cfg->deep_per_warp < 0 || cfg->readback_mib < 0)
         return fail(ctx, GLS_EINVAL, "invalid gls_config field");
     ctx->cfg = *cfg;
+    ctx->deep_per_warp = 0;                  // re-derived from cfg at the next simulate
     return GLS_OK;
 }
 
@@ -527,6 +550,8 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
     if (G) {
         CK(cudaMemcpy(ctx->d_gate.p, ginfo.data(), sizeof(GateInfo) * G, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_perm.p, perm.data(), sizeof(uint32_t) * G, cudaMemcpyHostToDevice));
+        CK(ctx->d_inv.alloc(G));
+        CK(cudaMemcpy(ctx->d_inv.p, inv.data(), sizeof(uint32_t) * G, cudaMemcpyHostToDevice));
     }
     if (E) {
         CK(cudaMemcpy(ctx->d_pin_src.p, psrc.data(), sizeof(uint32_t) * E, cudaMemcpyHostToDevice));
@@ -557,32 +582,71 @@ static int set_inputs_common(gls_ctx* ctx, int32_t P, int64_t total) {
     return GLS_OK;
 }
 
+// The per-transition rules (a2) checked on the device, on a copy that is not yet the
+// context's: host inputs are uploaded to a staging buffer (device inputs are checked in
+// place), and only a valid stimulus replaces the given waveforms in the arena prefix — a
+// rejected one leaves the previous inputs and result untouched (gls.h conventions).  If
+// the staging buffer cannot be allocated (HBM taken by the arena), the host inputs go
+// straight into the arena prefix and a rejected stimulus leaves no inputs (GLS_ESTATE at
+// the next simulate; stated in gls.h).
 static int upload_and_validate(gls_ctx* ctx, int32_t P, const int64_t* off, const uint64_t* tr, int64_t total,
                                cudaMemcpyKind kind) {
-    ctx->has_inputs = ctx->has_result = false;
-    ctx->window_active = false;
-    ctx->in_total = total;
-    ctx->prefix_total = 0;                 // nothing to keep while the new inputs are uploaded
-    int rc = ensure_arena(ctx, total + 1, false);
-    if (rc) return rc;
-    CK(ctx->d_in_off.alloc(P + 1));
-    CK(cudaMemcpyAsync(ctx->d_in_off.p, off, sizeof(int64_t) * (P + 1), kind, ctx->stream));
-    if (total) CK(cudaMemcpyAsync(ctx->d_arena.p, tr, sizeof(uint64_t) * total, kind, ctx->stream));
+    DevBuf<long long> st_off;
+    DevBuf<uint64_t> st_tr;
+    const long long* v_off = (const long long*)off;     // what is validated (device)
+    const uint64_t* v_tr = tr;
+    bool in_place = false;
+    if (kind == cudaMemcpyHostToDevice) {
+        CK(st_off.alloc((size_t)P + 1));
+        CK(cudaMemcpyAsync(st_off.p, off, sizeof(int64_t) * (P + 1), kind, ctx->stream));
+        v_off = st_off.p;
+        if (total) {
+            if (st_tr.alloc((size_t)total) != cudaSuccess) {
+                cudaGetLastError();
+                in_place = true;                        // no room for a staging copy
+            } else {
+                CK(cudaMemcpyAsync(st_tr.p, tr, sizeof(uint64_t) * total, kind, ctx->stream));
+                v_tr = st_tr.p;
+            }
+        }
+    }
+    if (in_place) {
+        ctx->has_inputs = ctx->has_result = false;
+        ctx->window_active = false;
+        ctx->prefix_total = 0;
+        int rc = ensure_arena(ctx, total + 1, false);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(ctx->d_arena.p, tr, sizeof(uint64_t) * total, kind, ctx->stream));
+        v_tr = ctx->d_arena.p;
+    }
     CK(cudaMemsetAsync(ctx->d_flag.p, 0, sizeof(unsigned) * 4, ctx->stream));
     CK(cudaMemsetAsync(ctx->d_flag64.p, 0, sizeof(unsigned long long) * 4, ctx->stream));
-    CK(launch_validate_inputs(P, ctx->d_in_off.p, ctx->d_arena.p, total, ctx->d_flag.p, ctx->d_flag64.p, ctx->stream));
+    CK(launch_validate_inputs(P, v_off, v_tr, total, ctx->d_flag.p, ctx->d_flag64.p, ctx->stream));
     unsigned err = 0;
     unsigned long long mt = 0;
     long long last_off = 0;
     CK(cudaMemcpyAsync(&err, ctx->d_flag.p, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(&mt, ctx->d_flag64.p, sizeof(mt), cudaMemcpyDeviceToHost, ctx->stream));
-    CK(cudaMemcpyAsync(&last_off, ctx->d_in_off.p + P, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&last_off, v_off + P, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (err || last_off != total)
         return fail(ctx, GLS_EINVAL,
                     "given waveforms invalid (%s%s%s)", (err & 1u) ? "bad offsets " : "",
                     (err & 2u) ? "times not strictly increasing / value repeats the previous one (first X) / time >= 2^61 " : "",
                     last_off != total ? "offsets[P] != total" : "");
+    // valid: it becomes the context's stimulus (arena prefix + offsets)
+    if (!in_place) {
+        ctx->has_inputs = ctx->has_result = false;
+        ctx->window_active = false;
+        ctx->prefix_total = 0;                          // nothing to keep while the arena is (re)sized
+        int rc = ensure_arena(ctx, total + 1, false);
+        if (rc) return rc;
+        if (total) CK(cudaMemcpyAsync(ctx->d_arena.p, v_tr, sizeof(uint64_t) * total, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    CK(ctx->d_in_off.ensure((size_t)P + 1));
+    CK(cudaMemcpyAsync(ctx->d_in_off.p, v_off, sizeof(int64_t) * (P + 1), cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->in_total = total;
     ctx->max_in_time = total ? (int64_t)mt : -1;
     ctx->prefix_total = total;
     ctx->has_inputs = true;
@@ -686,7 +750,7 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
     if (ctx->d_wscr.n < warp_scratch_entries(blocks)) CK(ctx->d_wscr.alloc(warp_scratch_entries(blocks)));
     const int64_t nwarps = (int64_t)blocks * (kThreads / 32);
     if (ctx->deep_per_warp == 0) ctx->deep_per_warp = ctx->cfg.deep_per_warp > 0 ? ctx->cfg.deep_per_warp : (1 << 16);
-    if ((int64_t)ctx->d_deep.n < nwarps * ctx->deep_per_warp) CK(ctx->d_deep.alloc(nwarps * ctx->deep_per_warp));
+    if ((int64_t)ctx->d_deep.n != nwarps * ctx->deep_per_warp) CK(ctx->d_deep.alloc(nwarps * ctx->deep_per_warp));
     if ((int64_t)ctx->d_deep_wtop.n < nwarps) CK(ctx->d_deep_wtop.alloc(nwarps));
 
     for (int attempt = 0; attempt < 3; ++attempt) {
@@ -715,7 +779,6 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
         CK(cudaStreamSynchronize(ctx->stream));
         const Ctl& c = ctx->last;
         ctx->last_chunk_top = std::max<unsigned long long>(c.chunk_top, ctx->last_chunk_top);
-        if (c.error & kErrBug) return fail(ctx, GLS_ECUDA, "internal consistency check failed (pass counts differ)");
         if (c.error & kErrWatchdog)
             return fail(ctx, GLS_ECUDA, "dataflow scheduler watchdog: no gate completed for 10 s (%llu of %d done)",
                         c.done_gates, ctx->G);
@@ -750,6 +813,7 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
             }
             if (retried) continue;
         }
+        if (c.error & kErrBug) return fail(ctx, GLS_ECUDA, "internal consistency check failed (pass counts differ)");
         // success
         float ms_k = 0, ms_s = 0;
         cudaEventElapsedTime(&ms_k, ctx->ev[1], ctx->ev[2]);
@@ -823,45 +887,95 @@ int gls_get_net_counts(gls_ctx* ctx, int64_t* counts) {
     return GLS_OK;
 }
 
+// a10 / GK3: the canonical CSR is built on the device (range_gather_kernel: every net's
+// chunk segments in time order, user net order) through a bounded staging buffer, batch
+// by batch of nets, each batch one D2H into the caller's array.
 int gls_get_waveforms(gls_ctx* ctx, int64_t* offsets, uint64_t* tr, int64_t capacity, int64_t* total_out) {
     if (!ctx) return GLS_EINVAL;
     if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    cudaSetDevice(ctx->device);
     const int64_t N = (int64_t)ctx->P + ctx->G;
     std::vector<unsigned long long> len((size_t)N);
-    std::vector<uint32_t> nck((size_t)N), nck_n((size_t)N);
-    if (N) {
-        CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(nck.data(), ctx->d_net_ck.p, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(nck_n.data(), ctx->d_net_nck.p, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost));
-    }
+    if (N) CK(cudaMemcpy(len.data(), ctx->d_net_len.p, sizeof(unsigned long long) * N, cudaMemcpyDeviceToHost));
     auto internal = [&](int64_t u) -> int64_t { return u < ctx->P ? u : ctx->P + ctx->inv[u - ctx->P]; };
-    int64_t total = 0;
-    for (int64_t u = 0; u < N; ++u) {
-        if (offsets) offsets[u] = total;
-        total += (int64_t)len[(size_t)internal(u)];
-    }
-    if (offsets) offsets[N] = total;
+    std::vector<int64_t> off((size_t)N + 1, 0);
+    for (int64_t u = 0; u < N; ++u) off[u + 1] = off[u] + (int64_t)len[(size_t)internal(u)];
+    const int64_t total = off[N];
+    if (offsets) std::memcpy(offsets, off.data(), sizeof(int64_t) * (N + 1));
     if (total_out) *total_out = total;
     if (!tr) return GLS_OK;
     if (capacity < total) return fail(ctx, GLS_ERANGE, "capacity %lld < %lld transitions", (long long)capacity, (long long)total);
-    const size_t nchunks = (size_t)ctx->last.chunk_top;
-    std::vector<unsigned long long> ck_off(nchunks);
-    std::vector<uint32_t> ck_cnt(nchunks);
-    if (nchunks) {
-        CK(cudaMemcpy(ck_off.data(), ctx->d_ck_off.p, sizeof(unsigned long long) * nchunks, cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(ck_cnt.data(), ctx->d_ck_cnt.p, sizeof(uint32_t) * nchunks, cudaMemcpyDeviceToHost));
+    if (total == 0) return GLS_OK;
+    int64_t maxlen = 0;
+    for (int64_t u = 0; u < N; ++u) maxlen = std::max<int64_t>(maxlen, off[u + 1] - off[u]);
+    const int64_t mib = ctx->cfg.readback_mib > 0 ? ctx->cfg.readback_mib : 1024;
+    const int64_t stage = std::min<int64_t>(total, std::max<int64_t>(maxlen, mib << 17));   // MiB / 8 B
+    DevBuf<uint64_t> d_stage;
+    DevBuf<long long> d_off;
+    CK(d_stage.alloc((size_t)stage));
+    CK(d_off.alloc((size_t)N + 1));
+    const SimParams p = params(ctx);
+    for (int64_t u0 = 0; u0 < N;) {
+        int64_t u1 = u0;                               // nets [u0, u1) fit the staging buffer
+        while (u1 < N && off[u1 + 1] - off[u0] <= stage) ++u1;
+        std::vector<long long> rel((size_t)(u1 - u0) + 1);
+        for (int64_t u = u0; u <= u1; ++u) rel[(size_t)(u - u0)] = off[u] - off[u0];
+        CK(cudaMemcpyAsync(d_off.p, rel.data(), sizeof(long long) * rel.size(), cudaMemcpyHostToDevice, ctx->stream));
+        CK(launch_range_gather(p, ctx->d_inv.p, u0, u1, LLONG_MIN, LLONG_MAX, d_off.p, d_stage.p, ctx->stream));
+        CK(cudaMemcpyAsync(tr + off[u0], d_stage.p, sizeof(uint64_t) * (off[u1] - off[u0]), cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        u0 = u1;
     }
-    std::vector<uint64_t> arena((size_t)ctx->last.arena_top);
-    if (!arena.empty())
-        CK(cudaMemcpy(arena.data(), ctx->d_arena.p, sizeof(uint64_t) * arena.size(), cudaMemcpyDeviceToHost));
-    int64_t o = 0;
-    for (int64_t u = 0; u < N; ++u) {
-        int64_t n = internal(u);
-        for (uint32_t j = nck[n]; j < nck[n] + nck_n[n]; ++j) {
-            std::memcpy(tr + o, arena.data() + ck_off[j], sizeof(uint64_t) * ck_cnt[j]);
-            o += ck_cnt[j];
-        }
+    return GLS_OK;
+}
+
+int gls_get_waveforms_range_device(gls_ctx* ctx, int64_t net_lo, int64_t net_hi, int64_t t_lo, int64_t t_hi,
+                                   int64_t* d_offsets, uint64_t* d_tr, int64_t capacity, int64_t* total_out) {
+    if (!ctx) return GLS_EINVAL;
+    if (!ctx->has_result) return fail(ctx, GLS_ESTATE, "no simulation result");
+    const int64_t N = (int64_t)ctx->P + ctx->G;
+    if (net_lo < 0 || net_hi < net_lo || net_hi > N) return fail(ctx, GLS_EINVAL, "net range [%lld, %lld) invalid",
+                                                                 (long long)net_lo, (long long)net_hi);
+    if (t_hi < t_lo) return fail(ctx, GLS_EINVAL, "t_hi < t_lo");
+    if (!d_offsets) return fail(ctx, GLS_EINVAL, "null offsets");
+    cudaSetDevice(ctx->device);
+    const int64_t n = net_hi - net_lo;
+    const SimParams p = params(ctx);
+    long long* o = (long long*)d_offsets;
+    CK(cudaMemsetAsync(o, 0, sizeof(long long), ctx->stream));
+    long long total = 0;
+    if (n > 0) {
+        DevBuf<long long> cnt;
+        CK(cnt.alloc((size_t)n));
+        CK(launch_range_counts(p, ctx->d_inv.p, net_lo, net_hi, t_lo, t_hi, cnt.p, ctx->stream));
+        size_t tb = 0;
+        CK(launch_inclusive_scan(cnt.p, o + 1, n, nullptr, &tb, ctx->stream));
+        DevBuf<unsigned char> tmp;
+        CK(tmp.alloc(tb));
+        CK(launch_inclusive_scan(cnt.p, o + 1, n, tmp.p, &tb, ctx->stream));
+        CK(cudaMemcpyAsync(&total, o + n, sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
+    if (total_out) *total_out = total;
+    if (!d_tr) {
+        CK(cudaStreamSynchronize(ctx->stream));
+        return GLS_OK;
+    }
+    if (capacity < total) return fail(ctx, GLS_ERANGE, "capacity %lld < %lld transitions", (long long)capacity, total);
+    CK(launch_range_gather(p, ctx->d_inv.p, net_lo, net_hi, t_lo, t_hi, o, d_tr, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return GLS_OK;
+}
+
+int gls_scatter_segments(gls_ctx* ctx, int64_t nseg, const int64_t* d_src_off, const uint64_t* d_src,
+                         const int64_t* d_dst_off, uint64_t* d_dst) {
+    if (!ctx) return GLS_EINVAL;
+    if (nseg < 0 || (nseg > 0 && (!d_src_off || !d_src || !d_dst_off || !d_dst)))
+        return fail(ctx, GLS_EINVAL, "bad segment arrays");
+    cudaSetDevice(ctx->device);
+    CK(launch_scatter_segments(nseg, (const long long*)d_src_off, d_src, (const long long*)d_dst_off, d_dst, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return GLS_OK;
 }
 

@@ -101,7 +101,7 @@ struct SimParams {
     long long duration;
     int32_t M;                  // target merged input events per chunk
     int32_t ring_cap;           // <= kRing
-    int32_t engine;             // 0 = lane slices, 1 = per-lane chunks, 2 = warp tiles
+    int32_t engine;             // 0 = lanes on re-balanced units, 1 = per-lane chunks
     int32_t sched;              // 0 = dataflow (ready counters), 1 = level barriers
     uint32_t nblocks;
 };
@@ -128,6 +128,16 @@ cudaError_t launch_hash_terms(const SimParams& p, const uint32_t* perm, long lon
 // sum over nets of len[n] * fanout[n] (fan-in reads of Alg. 2, for gls_stats.alg_bytes) into *out
 cudaError_t launch_fanin_reads(const unsigned long long* len, const uint32_t* fanout, long long n,
                                unsigned long long* out, cudaStream_t s);
+// canonical CSR of user nets [u0, u1) restricted to t_lo <= t <= t_hi: per-net counts, then
+// the gather into dst at the given (relative) offsets; generic segment scatter (stitching)
+cudaError_t launch_range_counts(const SimParams& p, const uint32_t* inv, long long u0, long long u1, long long t_lo,
+                                long long t_hi, long long* cnt, cudaStream_t s);
+cudaError_t launch_range_gather(const SimParams& p, const uint32_t* inv, long long u0, long long u1, long long t_lo,
+                                long long t_hi, const long long* off, uint64_t* dst, cudaStream_t s);
+cudaError_t launch_scatter_segments(long long nseg, const long long* src_off, const uint64_t* src,
+                                    const long long* dst_off, uint64_t* dst, cudaStream_t s);
+cudaError_t launch_inclusive_scan(const long long* in, long long* out, long long n, void* tmp, size_t* tmp_bytes,
+                                  cudaStream_t s);
 cudaError_t launch_hashes_window(const SimParams& p, const uint32_t* perm, long long t_lo, long long t_hi,
                                  uint64_t* out, cudaStream_t s);
 

@@ -13,12 +13,14 @@
 //     from one queue, so no warp ever waits for a level to drain;
 //   * level barriers: plan a topological level, device-wide barrier, evaluate
 //     it, barrier (kept for A/B and for the per-lane engine).
-// Three evaluation engines (gls_config.engine): 0 lanes on balanced time slices
-// of one chunk per warp (gls_slice.cuh), 1 one chunk per lane (below), 2
-// warp-cooperative tiles (gls_warp.cuh).  DESIGN.md §4-§5 give the derivations;
+// Two evaluation engines (gls_config.engine): 0 a warp's lanes on time-slice units
+// of a batch of chunks, re-balanced while they run (gls_lanes.cuh), 1 one chunk per
+// lane (below; also the exact fallback of engine 0).  DESIGN.md §4-§5 give the derivations;
 // every engine / scheduler is checked bit-exactly against oracle/ by
 // tests/test_gpu_parity.py.
 #include <climits>
+
+#include <cub/device/device_scan.cuh>
 
 #include "gls_internal.cuh"
 
@@ -27,17 +29,30 @@ namespace gls {
 // ------------------------------------------------------------------ helpers
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
     unsigned v;
+#ifndef GLS_NOFENCE
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#else
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+#endif
     return v;
 }
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// Counters whose last arriver reads what every earlier arriver wrote (gate completion,
+// the Alg. 1 ready counters): each arrival is a release RMW; only the last arriver then
+// issues an acquire fence (the fence-based acquire pattern of the PTX memory model), so
+// the L1 invalidation an acquire implies happens once per gate, not once per arrival.
 __device__ __forceinline__ unsigned atom_add_release(unsigned* p, unsigned v) {
     unsigned r;
     asm volatile("atom.add.release.gpu.global.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
     return r;
 }
+#ifndef GLS_NOFENCE
+__device__ __forceinline__ void fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+#else   // A/B only: no acquire (relaxed + L2 loads, control dependency)
+__device__ __forceinline__ void fence_acquire() {}
+#endif
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
     unsigned v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -221,7 +236,7 @@ __device__ void locate(const SimParams& p, uint32_t net, long long tau0, Cursor&
 struct ChunkSetup {
     uint32_t src[4];
     uint4 d[4];
-    uint32_t k, lut_base, dmin, dmax;
+    uint32_t k, lut_base, dmin, dmax, pin_off;
     long long T0, T1, tau0;
 };
 
@@ -447,6 +462,7 @@ __device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetu
     const uint32_t c = (uint32_t)(id - base);
     s.k = g.k;
     s.lut_base = g.lut_base;
+    s.pin_off = g.pin_off;
     unsigned long long lenref = 0, n_in = 0;
     uint32_t ref = 0;
     uint32_t dmin = 0xffffffffu, dmax = 0;
@@ -554,6 +570,7 @@ __device__ void process_level(const SimParams& p, unsigned long long ck_begin, u
             // descriptor is visible before the gate's done counter moves
             const unsigned prev = atom_add_release(&p.gate_done[gi], 1u);
             if (prev == nch - 1) {
+                fence_acquire();
                 // last chunk of the gate: prefix counts + net length (strong loads
                 // read L2, never a stale L1 line)
                 const uint32_t base = __ldcg(&p.net_ck[p.P + gi]);
@@ -701,9 +718,11 @@ __device__ void gate_complete(const SimParams& p, uint32_t gi, uint32_t base, ui
         bool ready = false;
         if (e < f1) {
             cg = p.fo_gate[e];
-            ready = atom_add_release(&p.pend[cg], 0xffffffffu) == 1u;   // decrement
+            ready = atom_add_release(&p.pend[cg], 0xffffffffu) == 1u;   // decrement; the last one plans cg
         }
-        for (unsigned rb = __ballot_sync(0xffffffffu, ready); rb; rb &= rb - 1) {
+        const unsigned rdy = __ballot_sync(0xffffffffu, ready);
+        if (rdy) fence_acquire();                       // (every lane: plan_gate reads the fan-ins' lengths)
+        for (unsigned rb = rdy; rb; rb &= rb - 1) {
             const int src = __ffs(rb) - 1;
             plan_gate(p, __shfl_sync(0xffffffffu, cg, src));
         }
@@ -740,74 +759,24 @@ __device__ void chunk_done(const SimParams& p, unsigned long long id, const Chun
         }
     }
     prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (R.fits && prev == R.nch - 1)
+    if (R.fits && prev == R.nch - 1) {
+        if (R.nch > 1) fence_acquire();                 // (every lane: the last chunk reads the others' counts)
         gate_complete<DATAFLOW>(p, R.gi, __ldcg(&p.net_ck[p.P + R.gi]), R.nch);
+    }
     __syncwarp();
 }
 
 
 }  // namespace gls
-#include "gls_warp.cuh"
-namespace gls {
-
-// one chunk with the warp-cooperative tile engine (whole warp)
-__device__ void process_chunk_warp(const SimParams& p, unsigned long long id, const uint8_t* lut, wv::WS& ws,
-                                   ChunkResult& R) {
-    const int lane = threadIdx.x & 31;
-    uint32_t c = 0;
-    setup_chunk(p, id, R.s, R.gi, c, R.nch);
-    uint64_t* scr = p.wscr + (size_t)warp_global_id() * wv::OBG;
-    unsigned long long off = 0, ev = 0, evt = 0;
-    uint32_t cnt = 0, vb = 2;
-    bool fits = true;
-    const bool ok = wv::warp_chunk(p, ws, scr, R.s, lut, off, cnt, vb, ev, evt, fits);
-    if (!ok) {
-        if (lane == 0) {
-            atomicAdd(&p.ctl->deep_chunks, 1ull);
-            lane_chunk(p, R.s, lut, off, cnt, vb, ev, evt, fits);
-        }
-        off = __shfl_sync(0xffffffffu, off, 0);
-        cnt = __shfl_sync(0xffffffffu, cnt, 0);
-        vb = __shfl_sync(0xffffffffu, vb, 0);
-        ev = __shfl_sync(0xffffffffu, ev, 0);
-        evt = __shfl_sync(0xffffffffu, evt, 0);
-        fits = __shfl_sync(0xffffffffu, (int)fits, 0) != 0;
-    } else {
-        ev = warp_sum64(ev);
-        evt = warp_sum64(evt);
-    }
-    R.off = off;
-    R.total = cnt;
-    R.vb = vb;
-    R.evals = ev;
-    R.events = evt;
-    R.fits = fits;
-}
-
-}  // namespace gls
-#include "gls_slice.cuh"
+#include "gls_lanes.cuh"
 namespace gls {
 
 #ifndef GLS_MINB
 #define GLS_MINB 3
 #endif
-constexpr int kDtabWords = 24;   // per-thread delay table words (slice engine)
-constexpr unsigned kEmpty = 0xffffffffu;
-
-// slice engine shared memory: per-thread delay tables, one Batch per warp, then the
-// per-thread pin cursors of the 32-bit sweep ([pin][thread] columns)
-__device__ __forceinline__ sl::Batch& slice_batch_smem(unsigned char* s_dyn) {
-    return reinterpret_cast<sl::Batch*>(s_dyn + (size_t)kDtabWords * kThreads * 2)[threadIdx.x >> 5];
-}
-__device__ __forceinline__ sl::PinSm pin_smem(unsigned char* s_dyn) {
-    return sl::PinSm{(uint32_t)__cvta_generic_to_shared(s_dyn + (size_t)kDtabWords * kThreads * 2 +
-                                                        sl::kBatchBytes * (kThreads / 32))};
-}
-
 template <int ENGINE, bool DATAFLOW>
-__global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
-    __shared__ uint8_t s_lut[kLutBytes];
-    extern __shared__ __align__(16) unsigned char s_dyn[];
+__global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(const __grid_constant__ SimParams p) {
+    uint8_t* const s_lut = ln::g_lut;
     for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) s_lut[i] = p.lut[i];
     __syncthreads();
     const int lane = threadIdx.x & 31;
@@ -817,84 +786,27 @@ __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(SimParams p) {
     if (DATAFLOW) {
         // seed: gates fed only by given nets (topological level 1) are ready now
         for (int g = (int)gwarp; g < p.level_off[1]; g += (int)nwarps) plan_gate(p, (uint32_t)g);
-        if (ENGINE == 0) {
-            unsigned long long carry = ~0ull;
-            if (lane == 0) sl::acc_zero(slice_batch_smem(s_dyn));
-            while (sl::slice_batch<true>(p, s_lut, reinterpret_cast<uint16_t*>(s_dyn), slice_batch_smem(s_dyn),
-                                         carry, 0, 0, nullptr, pin_smem(s_dyn))) {
-            }
-            if (lane == 0) sl::acc_flush(p, slice_batch_smem(s_dyn));
-        } else {
         // pull published chunks until every gate is complete (Alg. 1 loop)
-        for (;;) {
-            unsigned long long id = 0;
-            unsigned g = kEmpty;
-            if (lane == 0) {
-                id = atomicAdd(&p.ctl->work_head, 1ull);
-                unsigned ns = 32;
-                unsigned long long t_start = 0, seen = ~0ull;
-                for (;;) {
-                    if (id < p.ck_cap) {
-                        g = ld_relaxed_u32(&p.ck_gate[id]);
-                        if (g != kEmpty) break;
-                    }
-                    const unsigned long long done = ld_relaxed_u64(&p.ctl->done_gates);
-                    if (done >= (unsigned long long)p.G || ld_relaxed_u32(&p.ctl->error) != 0u) break;
-                    // watchdog: no gate completed anywhere for 10 s -> report instead of hanging
-                    unsigned long long now;
-                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-                    if (done != seen) {
-                        seen = done;
-                        t_start = now;
-                    } else if (now - t_start > 10000000000ull) {
-                        atomicOr(&p.ctl->error, kErrWatchdog);
-                        break;
-                    }
-                    __nanosleep(ns);
-                    if (ns < 8192) ns <<= 1;
-                }
-                p.deep_wtop[gwarp] = 0;                 // this warp's deep scratch, reused per chunk
-            }
-            g = __shfl_sync(0xffffffffu, g, 0);
-            id = __shfl_sync(0xffffffffu, id, 0);
-            if (g == kEmpty) return;
-            __syncwarp();
-            ChunkResult R;
-            process_chunk_warp(p, id, s_lut, reinterpret_cast<wv::WS*>(s_dyn)[threadIdx.x >> 5], R);
-            chunk_done<true>(p, id, R);
+        unsigned long long carry = ~0ull;
+        if (lane == 0) ln::acc_zero(ln::warp_batch());
+        while (ln::lane_batch<true>(p, carry, 0, 0, nullptr)) {
         }
-        }
+        if (lane == 0) ln::acc_flush(p, ln::warp_batch());
     } else {
         unsigned gen = 0;
         unsigned long long ck_begin = (unsigned long long)p.P;
-        if (ENGINE == 0 && lane == 0) sl::acc_zero(slice_batch_smem(s_dyn));
+        if (ENGINE == 0 && lane == 0) ln::acc_zero(ln::warp_batch());
         for (int l = 1; l <= p.L; ++l) {
             plan_level(p, l, gwarp, nwarps);
             if (grid_barrier(p.ctl, p.nblocks, gen)) return;
             const unsigned long long ck_end = *(volatile unsigned long long*)&p.ctl->chunk_top;
             if (ENGINE == 1) {
                 process_level(p, ck_begin, ck_end, &p.work[l], s_lut);
-            } else if (ENGINE == 0) {
-                unsigned long long carry = ~0ull;
-                while (sl::slice_batch<false>(p, s_lut, reinterpret_cast<uint16_t*>(s_dyn), slice_batch_smem(s_dyn),
-                                              carry, ck_begin, ck_end - ck_begin, &p.work[l], pin_smem(s_dyn))) {
-                }
-                if (lane == 0) sl::acc_flush(p, slice_batch_smem(s_dyn));   // (before the barrier: counts are read after it)
             } else {
-                const unsigned long long n = ck_end - ck_begin;
-                for (;;) {
-                    unsigned long long wb = 0;
-                    if (lane == 0) {
-                        wb = atomicAdd(&p.work[l], 1ull);
-                        p.deep_wtop[gwarp] = 0;
-                    }
-                    wb = __shfl_sync(0xffffffffu, wb, 0);
-                    if (wb >= n) break;
-                    __syncwarp();
-                    ChunkResult R;
-                    process_chunk_warp(p, ck_begin + wb, s_lut, reinterpret_cast<wv::WS*>(s_dyn)[threadIdx.x >> 5], R);
-                    chunk_done<false>(p, ck_begin + wb, R);
+                unsigned long long carry = ~0ull;
+                while (ln::lane_batch<false>(p, carry, ck_begin, ck_end - ck_begin, &p.work[l])) {
                 }
+                if (lane == 0) ln::acc_flush(p, ln::warp_batch());   // (before the barrier: counts are read after it)
             }
             if (grid_barrier(p.ctl, p.nblocks, gen)) return;
             ck_begin = ck_end;
@@ -1111,6 +1023,62 @@ __global__ void hash_terms_kernel(SimParams p, const uint32_t* perm, long long t
     }
 }
 
+
+// ------------------------------------------------------------------ result readback (a10, GK3)
+// Canonical CSR on the device: user nets [u0, u1) in net order, each net's transitions
+// with t_lo <= t <= t_hi (the whole run: LLONG_MIN, LLONG_MAX), gathered from its chunk
+// segments.  The paper transfers the finished store to the CPU as the output;
+// here the store is permuted into the caller's order on the device first, so the host
+// receives one contiguous CSR (or a device consumer — NCCL stitching — reads it).
+__device__ __forceinline__ uint32_t internal_net(const SimParams& p, const uint32_t* inv, long long u) {
+    return u < p.P ? (uint32_t)u : (uint32_t)p.P + inv[u - p.P];
+}
+__device__ __forceinline__ void net_range(const SimParams& p, uint32_t n, long long t_lo, long long t_hi,
+                                          unsigned long long& i0, unsigned long long& i1) {
+    i0 = t_lo == LLONG_MIN ? 0ull : count_before(p, n, t_lo);
+    i1 = t_hi == LLONG_MAX ? (unsigned long long)p.net_len[n] : count_before(p, n, t_hi + 1);
+    if (i1 < i0) i1 = i0;
+}
+__global__ void range_counts_kernel(SimParams p, const uint32_t* inv, long long u0, long long u1, long long t_lo,
+                                    long long t_hi, long long* cnt) {
+    for (long long u = u0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; u < u1;
+         u += (long long)gridDim.x * blockDim.x) {
+        unsigned long long i0, i1;
+        net_range(p, internal_net(p, inv, u), t_lo, t_hi, i0, i1);
+        cnt[u - u0] = (long long)(i1 - i0);
+    }
+}
+// one warp per net: coalesced copy of the net's [i0, i1) across its chunk segments
+__global__ void range_gather_kernel(SimParams p, const uint32_t* inv, long long u0, long long u1, long long t_lo,
+                                    long long t_hi, const long long* off, uint64_t* dst) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long u = u0 + (((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5); u < u1; u += nw) {
+        const uint32_t n = internal_net(p, inv, u);
+        unsigned long long i0, i1;
+        net_range(p, n, t_lo, t_hi, i0, i1);
+        uint64_t* d = dst + off[u - u0];
+        const uint32_t cb = p.net_ck[n], nck = p.net_nck[n];
+        for (uint32_t j = cb; j < cb + nck && i1 > i0; ++j) {
+            const unsigned long long c0 = p.ck_cum[j], c = p.ck_cnt[j];
+            if (c0 + c <= i0 || c0 >= i1) continue;    // chunk outside the range
+            const uint64_t* s = p.arena + p.ck_off[j];
+            const unsigned long long qa = i0 > c0 ? i0 - c0 : 0ull, qb = min(c, i1 - c0);
+            for (unsigned long long q = qa + lane; q < qb; q += 32) d[c0 + q - i0] = __ldcs(s + q);
+        }
+    }
+}
+// segment i (src_off[i] .. src_off[i+1]) -> dst + dst_off[i]; one warp per segment
+__global__ void scatter_segments_kernel(long long nseg, const long long* src_off, const uint64_t* src,
+                                        const long long* dst_off, uint64_t* dst) {
+    const int lane = threadIdx.x & 31;
+    const long long nw = ((long long)gridDim.x * blockDim.x) >> 5;
+    for (long long i = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nseg; i += nw) {
+        const long long a = src_off[i], b = src_off[i + 1], o = dst_off[i];
+        for (long long q = a + lane; q < b; q += 32) dst[o + (q - a)] = src[q];
+    }
+}
+
 // sum over nets of len x fan-out (measurement only)
 __global__ void fanin_reads_kernel(const unsigned long long* len, const uint32_t* fo, long long n,
                                    unsigned long long* out) {
@@ -1123,18 +1091,15 @@ __global__ void fanin_reads_kernel(const unsigned long long* len, const uint32_t
 
 // ------------------------------------------------------------------ launchers
 static size_t dyn_smem(int engine) {
-    return engine == 2 ? wv::kSmemBytes
-                       : (engine == 0 ? (size_t)kDtabWords * kThreads * 2 + sl::kBatchBytes * (kThreads / 32) + sl::kPinSmBytes
-                                      : 0);
+    return engine == 0 ? ln::kDynBytes : 0;
 }
 static const void* kernel_for(int engine, int sched) {
     if (engine == 1) return (const void*)sim_kernel<1, false>;
-    if (engine == 2) return sched == 1 ? (const void*)sim_kernel<2, false> : (const void*)sim_kernel<2, true>;
     return sched == 1 ? (const void*)sim_kernel<0, false> : (const void*)sim_kernel<0, true>;
 }
 
 size_t warp_scratch_entries(int blocks) {
-    return (size_t)blocks * (kThreads / 32) * (wv::OBG > (int)sl::kScratchPerWarp ? (size_t)wv::OBG : sl::kScratchPerWarp);
+    return (size_t)blocks * (kThreads / 32) * ln::kScratchPerWarp;
 }
 
 int max_coresident_blocks(int device, int engine, int sched, int* per_sm) {
@@ -1201,6 +1166,36 @@ cudaError_t launch_hash_terms(const SimParams& p, const uint32_t* perm, long lon
     return cudaGetLastError();
 }
 
+cudaError_t launch_range_counts(const SimParams& p, const uint32_t* inv, long long u0, long long u1, long long t_lo,
+                                long long t_hi, long long* cnt, cudaStream_t s) {
+    if (u1 <= u0) return cudaSuccess;
+    long long blocks = (u1 - u0 + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    range_counts_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, inv, u0, u1, t_lo, t_hi, cnt);
+    return cudaGetLastError();
+}
+cudaError_t launch_range_gather(const SimParams& p, const uint32_t* inv, long long u0, long long u1, long long t_lo,
+                                long long t_hi, const long long* off, uint64_t* dst, cudaStream_t s) {
+    if (u1 <= u0) return cudaSuccess;
+    long long blocks = (u1 - u0 + 7) / 8;              // one warp per net
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    range_gather_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, inv, u0, u1, t_lo, t_hi, off, dst);
+    return cudaGetLastError();
+}
+cudaError_t launch_scatter_segments(long long nseg, const long long* src_off, const uint64_t* src,
+                                    const long long* dst_off, uint64_t* dst, cudaStream_t s) {
+    if (nseg <= 0) return cudaSuccess;
+    long long blocks = (nseg + 7) / 8;                 // one warp per segment
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    scatter_segments_kernel<<<(unsigned)blocks, 256, 0, s>>>(nseg, src_off, src, dst_off, dst);
+    return cudaGetLastError();
+}
+
+// inclusive prefix sum (CUB); tmp == NULL: *tmp_bytes = the scratch it needs
+cudaError_t launch_inclusive_scan(const long long* in, long long* out, long long n, void* tmp, size_t* tmp_bytes,
+                                  cudaStream_t s) {
+    return cub::DeviceScan::InclusiveSum(tmp, *tmp_bytes, in, out, (int64_t)n, s);
+}
 cudaError_t launch_fanin_reads(const unsigned long long* len, const uint32_t* fanout, long long n,
                                unsigned long long* out, cudaStream_t s) {
     if (n <= 0) return cudaSuccess;

@@ -24,7 +24,8 @@ EXPORTS = ["gls_create", "gls_destroy", "gls_last_error", "gls_version", "gls_se
            "gls_load_netlist", "gls_set_input_waveforms", "gls_set_input_waveforms_device",
            "gls_simulate", "gls_simulate_window", "gls_get_waveforms", "gls_get_net_hashes", "gls_get_net_hashes_device",
            "gls_get_net_hashes_window", "gls_get_net_hash_terms_device",
-           "gls_get_net_counts", "gls_get_stats", "gls_get_halo", "gls_get_levels", "gls_lut_lookup"]
+           "gls_get_net_counts", "gls_get_stats", "gls_get_halo", "gls_get_levels", "gls_lut_lookup",
+           "gls_get_waveforms_range_device", "gls_scatter_segments"]
 
 
 class GlsError(RuntimeError):
@@ -37,7 +38,7 @@ class gls_config(ctypes.Structure):
     _fields_ = [("arena_bytes", ctypes.c_int64), ("chunk_capacity", ctypes.c_int64),
                 ("chunk_events", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
                 ("ring_limit", ctypes.c_int32), ("engine", ctypes.c_int32), ("scheduler", ctypes.c_int32),
-                ("deep_per_warp", ctypes.c_int64), ("reserved", ctypes.c_int32 * 2)]
+                ("deep_per_warp", ctypes.c_int64), ("readback_mib", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 class gls_stats(ctypes.Structure):
@@ -92,6 +93,8 @@ def load_library():
         "gls_get_halo": (ctypes.c_int, [vp, p(i64)]),
         "gls_get_levels": (ctypes.c_int, [vp, p(i32)]),
         "gls_lut_lookup": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, vp]),
+        "gls_get_waveforms_range_device": (ctypes.c_int, [vp, i64, i64, i64, i64, vp, vp, i64, p(i64)]),
+        "gls_scatter_segments": (ctypes.c_int, [vp, i64, vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -164,9 +167,9 @@ class Context:
 
     # ---- ABI calls ----------------------------------------------------------
     def gls_set_config(self, arena_bytes=0, chunk_capacity=0, chunk_events=0, blocks_per_sm=0, ring_limit=0,
-                       engine=0, scheduler=0, deep_per_warp=0):
+                       engine=0, scheduler=0, deep_per_warp=0, readback_mib=0):
         c = gls_config(arena_bytes, chunk_capacity, chunk_events, blocks_per_sm, ring_limit, engine, scheduler,
-                       deep_per_warp)
+                       deep_per_warp, readback_mib)
         return self._check(self._lib.gls_set_config(self._h, ctypes.byref(c)))
 
     def gls_load_netlist(self, num_inputs, gate_type, fanin_offsets, fanin_net, pin_delay):
@@ -207,6 +210,19 @@ class Context:
         self._check(self._lib.gls_get_waveforms(self._h, offs.ctypes.data, tr.ctypes.data, tr.size,
                                                 ctypes.byref(total)))
         return Waveforms(offs, tr[:total.value])
+
+    def gls_get_waveforms_range_device(self, net_lo, net_hi, t_lo, t_hi, d_offsets, d_trans=0, capacity=0) -> int:
+        """Device pointers (ints; d_trans 0 = size query).  Returns the transition count."""
+        total = ctypes.c_int64()
+        self._check(self._lib.gls_get_waveforms_range_device(
+            self._h, int(net_lo), int(net_hi), int(t_lo), int(t_hi), ctypes.c_void_p(d_offsets),
+            ctypes.c_void_p(d_trans) if d_trans else None, int(capacity), ctypes.byref(total)))
+        return total.value
+
+    def gls_scatter_segments(self, nseg, d_src_off, d_src, d_dst_off, d_dst):
+        vp = lambda x: ctypes.c_void_p(x) if x else None
+        return self._check(self._lib.gls_scatter_segments(self._h, int(nseg), vp(d_src_off), vp(d_src),
+                                                          vp(d_dst_off), vp(d_dst)))
 
     def gls_get_net_hashes(self) -> np.ndarray:
         h = np.zeros(self.num_inputs + self.num_gates, np.uint64)

@@ -92,3 +92,83 @@ def gls_window_stitch(ctx, own_lo, own_hi, device, group=None):
         return terms
 
     return stitch_hashes(counts, terms_fn, group)
+
+
+# ---------------------------------------------------------------- waveform stitching
+# SURVEY §8(e) "Stitch": all_gather the per-net counts of every rank's owned window ->
+# global offsets -> the rank segments go to the owner (point-to-point over NCCL / NVLink)
+# -> the owner scatters each rank's per-net runs into the canonical CSR on its device.
+
+def assemble(allc, bufs, scatter_fn, out_alloc):
+    """Owner side: canonical CSR from the ranks' window CSRs.
+
+    allc: [world, nets] int64 counts (rank r's transitions of net n in its window, the
+    windows in time order); bufs[r]: rank r's window CSR transitions (net order);
+    scatter_fn(nseg, src_off, src, dst_off, dst) copies segment i of src (src_off[i] ..
+    src_off[i+1]) to dst + dst_off[i].  Returns (offsets [nets+1], transitions)."""
+    world, n = allc.shape
+    total_n = allc.sum(0)
+    off = torch.zeros(n + 1, dtype=torch.int64, device=allc.device)
+    torch.cumsum(total_n, 0, out=off[1:])
+    out = out_alloc(int(off[-1]))
+    before = torch.zeros(n, dtype=torch.int64, device=allc.device)     # transitions of the net in earlier windows
+    for r in range(world):
+        src_off = torch.zeros(n + 1, dtype=torch.int64, device=allc.device)
+        torch.cumsum(allc[r], 0, out=src_off[1:])
+        scatter_fn(n, src_off, bufs[r], off[:-1] + before, out)
+        before += allc[r]
+    return off, out
+
+
+def stitch_waveforms(counts, buf, scatter_fn, out_alloc, dst=0, group=None):
+    """Every rank: counts [nets] (int64) and buf (its window CSR transitions, int64 bits);
+    the canonical CSR of the whole run on rank `dst` (None elsewhere)."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    allc = [torch.empty_like(counts) for _ in range(world)]
+    dist.all_gather(allc, counts, group=group)
+    allc = torch.stack(allc)
+    sizes = allc.sum(1).tolist()
+    if rank != dst:
+        if sizes[rank]:
+            dist.send(buf[:sizes[rank]].contiguous(), dst, group=group)
+        return None
+    bufs = []
+    for r in range(world):
+        if r == rank:
+            bufs.append(buf)
+        else:
+            b = torch.empty(max(1, sizes[r]), dtype=torch.int64, device=counts.device)
+            if sizes[r]:
+                dist.recv(b[:sizes[r]], r, group=group)
+            bufs.append(b)
+    return assemble(allc, bufs, scatter_fn, out_alloc)
+
+
+def gls_window_csr(ctx, own_lo, own_hi, device, net_lo=0, net_hi=None):
+    """This rank's owned window as a device CSR (gls_get_waveforms_range_device):
+    (counts [nets], transitions)."""
+    n_all = ctx.num_inputs + ctx.num_gates
+    net_hi = n_all if net_hi is None else net_hi
+    n = net_hi - net_lo
+    offs = torch.empty(n + 1, dtype=torch.int64, device=device)
+    total = ctx.gls_get_waveforms_range_device(net_lo, net_hi, own_lo, own_hi, offs.data_ptr())
+    tr = torch.empty(max(1, total), dtype=torch.int64, device=device)
+    ctx.gls_get_waveforms_range_device(net_lo, net_hi, own_lo, own_hi, offs.data_ptr(), tr.data_ptr(), tr.numel())
+    return offs[1:] - offs[:-1], tr
+
+
+def gls_scatter(ctx):
+    """scatter_fn running gls_scatter_segments on ctx's device."""
+    def fn(nseg, src_off, src, dst_off, dst):
+        ctx.gls_scatter_segments(nseg, src_off.data_ptr(), src.data_ptr(), dst_off.contiguous().data_ptr(),
+                                 dst.data_ptr())
+    return fn
+
+
+def gls_gather_waveforms(ctx, own_lo, own_hi, device, dst=0, group=None, net_lo=0, net_hi=None):
+    """Canonical CSR of nets [net_lo, net_hi) over the whole run on rank `dst` (device
+    tensors (offsets, transitions as int64 bits)), from the ranks' time windows."""
+    counts, tr = gls_window_csr(ctx, own_lo, own_hi, device, net_lo, net_hi)
+    return stitch_waveforms(counts, tr, gls_scatter(ctx),
+                            lambda k: torch.empty(max(1, k), dtype=torch.int64, device=device), dst, group)

@@ -144,6 +144,7 @@ class StimSpec:
     num_inputs: int
     ncycles: int
     epoch_len: np.ndarray = field(repr=False, default=None)  # int64 [P] (>=1)
+    hot: np.ndarray = field(repr=False, default=None)        # int64 [P]: 0, or toggles per cycle of a hot PI
 
     @property
     def duration(self) -> int:
@@ -151,20 +152,69 @@ class StimSpec:
         return self.ncycles * PERIOD + 1
 
 
+HOT_WCV_COLD = 3.0          # WCV of the epoch-toggling PIs when hot PIs carry the rest of the skew
+
+
+def _epochs(z, mean, w, ncycles):
+    """Lognormal epoch lengths (cycles, >= 1) for a target mean transition count and WCV."""
+    sigma = math.sqrt(math.log(1.0 + w * w))
+    c = mean * np.exp(sigma * z - 0.5 * sigma * sigma)
+    return np.clip(np.rint(0.5 * ncycles / np.maximum(c, 1e-9)), 1, ncycles).astype(np.int64)
+
+
+def _wcv_of(L, hot, ncycles):
+    """Expected per-PI transition counts (an epoch boundary changes the level with p ~ 1/2)."""
+    e = np.where(hot > 0, hot * ncycles, 0.5 * ncycles / L)
+    return float(e.std() / e.mean()), float(e.mean())
+
+
 def make_stimspec(seed, num_inputs, ncycles, profile="random", mean_trans=None, wcv=None) -> StimSpec:
+    hot = np.zeros(num_inputs, np.int64)
     if profile == "random":
         L = np.ones(num_inputs, np.int64)
     elif profile == "skewed":
         assert mean_trans and wcv
         rng = np.random.Generator(np.random.PCG64(seed + 7919))
-        sigma = math.sqrt(math.log(1.0 + wcv * wcv))
         z = rng.standard_normal(num_inputs)
-        c = mean_trans * np.exp(sigma * z - 0.5 * sigma * sigma)
-        L = np.rint(0.5 * ncycles / np.maximum(c, 1e-9))
-        L = np.clip(L, 1, ncycles).astype(np.int64)
+        L = _epochs(z, mean_trans, wcv, ncycles)
+        if _wcv_of(L, hot, ncycles)[0] < 0.9 * wcv:
+            # An epoch is >= 1 cycle, so one PI carries at most ~ncycles/2 transitions and
+            # a lognormal mix saturates (WCV ~6 at 1,000 per PI over 297k cycles).  The
+            # paper's skewed designs (WCV 17.1 and 54.5, P:530-532) need nets that toggle
+            # more than once per cycle: the most active PIs become clock-like (h toggles
+            # per cycle), the rest keep lognormal epochs (WCV 3), and the mean activity is
+            # held at mean_trans.  The number of hot PIs is set by bisection on the WCV.
+            order = np.argsort(-z, kind="stable")
+            best = None
+            for h in (1, 2, 4, 8, 16):
+                H = h * ncycles
+                hi_n = int(min(num_inputs // 4, mean_trans * num_inputs // H))
+
+                def at(nh):
+                    hh = np.zeros(num_inputs, np.int64)
+                    hh[order[:nh]] = h
+                    mc = (mean_trans * num_inputs - nh * H) / max(1, num_inputs - nh)
+                    Lc = _epochs(z, max(mc, 1e-3), HOT_WCV_COLD, ncycles)
+                    return hh, Lc, _wcv_of(Lc, hh, ncycles)[0]
+
+                if hi_n < 1:
+                    continue
+                if at(hi_n)[2] < wcv:
+                    best = at(hi_n)
+                    continue
+                lo_n = 0
+                while hi_n - lo_n > 1:               # smallest count reaching the target
+                    mid = (lo_n + hi_n) // 2
+                    if at(mid)[2] >= wcv:
+                        hi_n = mid
+                    else:
+                        lo_n = mid
+                best = at(hi_n)
+                break
+            hot, L, _ = best
     else:
         raise ValueError(profile)
-    return StimSpec(seed, num_inputs, ncycles, L)
+    return StimSpec(seed, num_inputs, ncycles, L, hot)
 
 
 def _pi_params(spec: StimSpec, pis: torch.Tensor):
@@ -218,12 +268,14 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
         p1 = min(P, max(p1, p0 + 1), p0 + pi_batch)
         bounds.append((p0, p1))
         p0 = p1
+    hot_all = torch.as_tensor(spec.hot if spec.hot is not None else np.zeros(P, np.int64), device=dev)
     for p0, p1 in bounds:
         pis = torch.arange(p0, p1, device=dev, dtype=torch.int64)
         L, off, phase = _pi_params(spec, pis)
         e_lo = _epoch_of_cycle(torch.full_like(pis, cycle_lo), L, phase)
         e_hi = _epoch_of_cycle(torch.full_like(pis, max(cycle_hi - 1, cycle_lo)), L, phase)
         n_ep = torch.where(torch.full_like(pis, cycle_hi) > cycle_lo, e_hi - e_lo + 1, torch.zeros_like(pis))
+        n_ep = torch.where(hot_all[p0:p1] > 0, torch.zeros_like(n_ep), n_ep)     # hot PIs: below
         tot = int(n_ep.sum().item())
         if tot == 0:
             continue
@@ -240,11 +292,40 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
         pi, k, cur, offr = pi[m], k[m], cur[m], offr[m]
         jit = _hash3(spec.seed, pi, k, _TAG_JIT) % 6
         t = k * PERIOD + offr + jit
-        chunks.append((t << 2) | cur)
+        chunks.append((pi, (t << 2) | cur))
         counts[p0:p0 + pis.numel()] += torch.bincount(pi - p0, minlength=pis.numel())
+    # hot (clock-like) PIs: h transitions per cycle at offset_i + j * PERIOD / h, the value
+    # alternating 0/1 from a per-PI start bit (never X: every transition changes the value)
+    hp = torch.nonzero(hot_all > 0).flatten()
+    if hp.numel() and cycle_hi > cycle_lo:
+        h = hot_all[hp]
+        k_hi = min(cycle_hi, spec.ncycles)
+        per = (k_hi - cycle_lo) * h
+        tot = int(per.sum().item())
+        if tot:
+            rep = torch.repeat_interleave(torch.arange(hp.numel(), device=dev), per)
+            start = torch.cumsum(per, 0) - per
+            n = torch.arange(tot, device=dev, dtype=torch.int64) - start[rep] + cycle_lo * h[rep]   # global index
+            hr = h[rep]
+            k = torch.div(n, hr, rounding_mode="floor")
+            j = n - k * hr
+            pi = hp[rep]
+            _, off, _ = _pi_params(spec, pi)
+            sb = _hash3(spec.seed, pi, torch.zeros_like(pi), _TAG_LVL) & 1
+            t = k * PERIOD + off + j * torch.div(torch.full_like(hr, PERIOD), hr, rounding_mode="floor")
+            chunks.append((pi, (t << 2) | ((sb + n) & 1)))
+            counts.index_add_(0, hp, per)
     offs = torch.zeros(P + 1, dtype=torch.int64, device=dev)
     offs[1:] = torch.cumsum(counts, 0)
-    trans = torch.cat(chunks) if chunks else torch.zeros(0, dtype=torch.int64, device=dev)
+    trans = torch.empty(int(offs[-1].item()), dtype=torch.int64, device=dev)
+    # every group holds whole PIs, each PI's entries time-sorted: scatter them to their CSR rows
+    for pi, e in chunks:
+        if pi.numel() == 0:
+            continue
+        first = torch.ones_like(pi, dtype=torch.bool)
+        first[1:] = pi[1:] != pi[:-1]
+        gstart = torch.cummax(torch.where(first, torch.arange(pi.numel(), device=dev), torch.zeros_like(pi)), 0)[0]
+        trans[offs[pi] + (torch.arange(pi.numel(), device=dev) - gstart)] = e
     return offs, trans
 
 
@@ -266,6 +347,10 @@ def window_stimuli(spec: StimSpec, cycle_lo: int, cycle_hi: int, device="cpu", p
     pis = torch.arange(P, device=dev, dtype=torch.int64)
     L, _, phase = _pi_params(spec, pis)
     lvl = _level(spec, pis, _epoch_of_cycle(torch.full_like(pis, cycle_lo - 1), L, phase))
+    if spec.hot is not None and (spec.hot > 0).any():
+        h = torch.as_tensor(spec.hot, device=dev)
+        sb = _hash3(spec.seed, pis, torch.zeros_like(pis), _TAG_LVL) & 1
+        lvl = torch.where(h > 0, (sb + min(cycle_lo, spec.ncycles) * h - 1) & 1, lvl)   # its last value
     has = lvl != 2
     nc = has.to(torch.int64)
     new_off = torch.zeros(P + 1, dtype=torch.int64, device=dev)

@@ -25,10 +25,10 @@ def run_oracle(nl, st, dur):
                            nl.pin_delay, st.offsets, st.trans, dur)
 
 
-# engine 0 = lane slices (default), 1 = per-lane chunks, 2 = warp-cooperative tiles;
+# engine 0 = lanes on re-balanced time-slice units (default), 1 = one chunk per lane;
 # scheduler 0 = dataflow (default), 1 = level barriers
-ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1), dict(engine=2), dict(engine=2, scheduler=1)]
-EIDS = ["slice-df", "slice-lvl", "lane", "warp-df", "warp-lvl"]
+ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1)]
+EIDS = ["units-df", "units-lvl", "lane"]
 
 
 def run_gpu(c, nl, st, dur, **cfg):
@@ -132,8 +132,8 @@ def test_large_times(ctx, engine):
 @pytest.mark.parametrize("engine", ENGINES[:2], ids=EIDS[:2])
 @pytest.mark.parametrize("lo,hi", [(5000, 5200), (0, 1000), (60000, 70000)])
 def test_delay_spread_paths(ctx, lo, hi, engine):
-    """Delays below 2^16 take the 32-bit sweep (u16 delay table), larger ones the 64-bit
-    sweep; both with large and small per-gate spreads."""
+    """Delays below 2^16 take the 32-bit sweep (u16 delay table), larger ones the per-lane
+    ring engine (fallback units); both with large and small per-gate spreads."""
     for seed in range(3):
         nl = W.random_dag(970 + seed, 5, 60, max_delay=hi, min_delay=lo)
         st = W.random_stimuli(seed, 5, 60, 40 * hi + 400, xz=0.2, max_gap=hi // 3 + 5)
@@ -144,7 +144,7 @@ def test_delay_spread_paths(ctx, lo, hi, engine):
 @pytest.mark.parametrize("seed", range(4))
 def test_rebase_boundaries(ctx, seed, engine):
     """Glitch-dense bursts straddling multiples of 2^29 ps: the 32-bit sweep moves its
-    time base there (gls_sweep.cuh) with schedules pending across the move."""
+    time base there (gls_lanes.cuh) with schedules pending across the move."""
     rng = np.random.Generator(np.random.PCG64(4000 + seed))
     nl = W.random_dag(950 + seed, 4, 40, max_delay=30)
     waves = []
@@ -195,7 +195,7 @@ def test_determinism_and_launch_shapes(ctx):
     ref = run_oracle(nl, st, spec.duration)
     base = None
     for cfg in [dict(), dict(blocks_per_sm=1), dict(chunk_events=32), dict(chunk_events=4096), dict(engine=1),
-                dict(engine=1, chunk_events=64), dict(engine=2), dict(engine=2, chunk_events=64),
+                dict(engine=1, chunk_events=64), dict(chunk_events=7), dict(chunk_events=64, blocks_per_sm=1),
                 dict(scheduler=1), dict(scheduler=1, chunk_events=64), dict(deep_per_warp=64), dict()]:
         w, _ = run_gpu(ctx, nl, st, spec.duration, **cfg)
         assert np.array_equal(w.trans, ref.trans)
@@ -297,22 +297,23 @@ def test_generator_cpu_equals_gpu():
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_warp_engine_deep_pending_and_spills(ctx, seed):
-    """Large delay spreads with dense events overflow the warp engine's pending
-    list (-> per-lane fallback); long single-chunk gates spill its output buffer."""
+def test_deep_pending_and_scratch_overflow(ctx, seed):
+    """Large delay spreads with dense events: long pending lists (the Eq. 1 stack; the
+    per-lane engine's ring -> deep path); long single-chunk gates overflow the lane
+    scratch (-> fallback units)."""
     nl = W.random_dag(1200 + seed, 4, 40, max_delay=400, min_delay=0)
     st = W.random_stimuli(seed, 4, 600, 3000, xz=0.05, min_gap=1, max_gap=3)
-    for eng in (0, 2):
+    for eng in (0, 1):
         for sch in (0, 1):
             assert_same(ctx, nl, st, 4000, engine=eng, scheduler=sch, chunk_events=1 << 20, hashes=False)
     nl = W.random_dag(1300 + seed, 3, 30, max_delay=2, types=[W.BUF, W.NOT, W.XOR])
     st = W.random_stimuli(seed, 3, 3000, 60000, xz=0.0, min_gap=5, max_gap=30)
-    for eng in (0, 2):
+    for eng in (0, 1):
         for sch in (0, 1):
             assert_same(ctx, nl, st, 61000, engine=eng, scheduler=sch, chunk_events=1 << 20, hashes=False)
 
 
-@pytest.mark.parametrize("engine", ENGINES[:2] + ENGINES[3:4], ids=EIDS[:2] + EIDS[3:4])
+@pytest.mark.parametrize("engine", ENGINES, ids=EIDS)
 def test_simulate_window_matches_full_run(ctx, engine):
     """gls_simulate_window (reading R17 inside the library): on [t_begin, t_end) the
     window run's transitions equal the full run's (oracle), for windows at the start,
