@@ -133,6 +133,20 @@ def build_netlist(cfg, seed):
     return nl
 
 
+def host_cpu():
+    """CPU model and logical core count of the host (the oracle timings' machine)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def oracle_sample(nl, spec, cycles):
     """The oracle as it stands on the workload's first `cycles` clock cycles."""
     from oracle import oracle
@@ -156,7 +170,10 @@ def run_reference(a):
     # split into time windows
     replicas = cfg == "c5_set" and world > 1
     spec = W.config_stimspec(cfg, a.seed + (rank if replicas else 0))
-    cyc = max(1, (a.sample_cycles or SAMPLE_CYCLES[cfg]) // 4)
+    # the cpu_baseline leg's sample when K + W = 8 (the default run), shorter for longer
+    # runs so that the whole reference arm stays within a few minutes
+    base = a.sample_cycles or SAMPLE_CYCLES[cfg]
+    cyc = max(1, base * 8 // max(8, a.steps + a.warmup))
     for _ in range(a.warmup):
         oracle_sample(nl, spec, cyc)
     evals, secs, outs = 0, 0.0, 0
@@ -174,7 +191,8 @@ def run_reference(a):
             "dtype": "int64", "data": "synthetic",
             "config": {"workload": cfg, "gates": nl.num_gates, "pis": nl.num_inputs},
             "output_transitions_per_s": outs / secs,
-            "cpu_baseline": {"value": v, "unit": "gate-evals/s", "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "gate-evals/s", "cores": 1, "kind": "oracle", "sample": sample,
+                             **host_cpu()},
             "e2e": {"value": v, "unit": "gate-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -187,6 +205,73 @@ def balance_str(s):
     nb = max(1, s.get("batches") or 1)
     return (f"[units/batch {b[0] / nb:.1f}, splits/batch {b[1] / nb:.2f}, rounds/batch {b[2] / nb:.1f}, "
             f"fallback units {int(b[3])}]")
+
+
+def post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_hashes, stims):
+    """N > 1, after the timed region: the §8(e) stitch of the ranks' results:
+    time windows — full-run per-net checksums and the waveforms of 1/16 of the nets
+    gathered on rank 0; stimulus sets — every set's per-net checksums on every rank."""
+    stitch = None
+    if world > 1 and not replicas:
+        from paper_2304_13398_b200 import shard as _shard
+        lo, hi = plan["own"]
+        torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        stitched = _shard.gls_window_stitch(ctx, lo, hi, dev)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        st_ms = s0.elapsed_time(s1)
+        tt = torch.tensor([st_ms], dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(tt) for _ in range(world)]
+        torch.distributed.all_gather(allv, tt)
+        stitch = {"ms": float(torch.stack(allv).max()), "nets": int(stitched.numel()),
+                  "bytes_per_rank": int(16 * stitched.numel()),
+                  "what": "full-run per-net checksums from the time windows (all_gather of counts and "
+                          "position-keyed terms over NCCL)"}
+        del stitched
+        # the waveforms themselves (§8(e) stitch): every rank's owned-window CSR of the first
+        # 1/16 of the nets to rank 0 (the whole result, ~90 GB, would not fit beside rank 0's
+        # own arena), assembled there into the canonical CSR of the full run
+        n_sub = max(1, nl.num_nets // 16)
+        torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        s0.record(stream)
+        res = _shard.gls_gather_waveforms(ctx, lo, hi, dev, dst=0, net_lo=0, net_hi=n_sub)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        g_ms = s0.elapsed_time(s1)
+        tt = torch.tensor([g_ms], dtype=torch.float64, device=dev)
+        allv = [torch.zeros_like(tt) for _ in range(world)]
+        torch.distributed.all_gather(allv, tt)
+        if rank == 0:
+            g_bytes = 8 * int(res[0][-1])
+            stitch["waveforms"] = {"ms": float(torch.stack(allv).max()), "nets": [0, n_sub], "bytes": g_bytes,
+                                   "gbs": g_bytes / (float(torch.stack(allv).max()) / 1e3) / 1e9,
+                                   "what": "owned-window CSRs (gls_get_waveforms_range_device) -> NCCL "
+                                           "send/recv to rank 0 -> gls_scatter_segments into the full-run CSR"}
+        del res
+    if world > 1 and replicas:
+        # C5: every set's per-net checksums (computed on the device in the step) to every rank
+        torch.distributed.barrier()
+        torch.cuda.synchronize(dev)
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        per = (C5_SETS + world - 1) // world
+        mine = torch.zeros((per, nl.num_nets), dtype=torch.int64, device=dev)
+        mine[:len(stims)] = set_hashes
+        allh = [torch.empty_like(mine) for _ in range(world)]
+        torch.distributed.all_gather(allh, mine)
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        # set k lives on rank k % world at row k // world
+        h0 = allh[0][0].cpu()
+        stitch = {"ms": s0.elapsed_time(s1), "sets": C5_SETS, "bytes": int(8 * per * world * nl.num_nets),
+                  "what": "per-set per-net checksums (device, in the step) all_gathered over NCCL",
+                  "set0_matches_rank0": bool(torch.equal(h0, set_hashes[0].cpu()))}
+        del allh, mine
+    return stitch
 
 
 def run_gls(a):
@@ -236,6 +321,7 @@ def run_gls(a):
         f"({time.perf_counter() - t:.1f}s)")
     if len(stims) == 1:
         ctx.gls_set_input_waveforms_device(nl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), n_in)
+    set_hashes = torch.zeros((len(stims), nl.num_nets), dtype=torch.int64, device=dev) if len(stims) > 1 else None
 
     def step():
         """One pass of the hot path over the rank's batch of input: its time window, or each
@@ -245,9 +331,10 @@ def run_gls(a):
             ctx.gls_simulate(duration)
             return [ctx.gls_get_stats()]
         out = []
-        for o_, t_, n_ in stims:
+        for k_, (o_, t_, n_) in enumerate(stims):
             ctx.gls_set_input_waveforms_device(nl.num_inputs, o_.data_ptr(), t_.data_ptr(), n_)
             ctx.gls_simulate(duration)
+            ctx.gls_get_net_hashes_device(set_hashes[k_].data_ptr())     # a10 per set, on the device
             out.append(ctx.gls_get_stats())
         return out
 
@@ -297,25 +384,11 @@ def run_gls(a):
     # (NCCL all_gather of per-net counts, then of position-keyed terms; shard.stitch_hashes),
     # timed on the device after the timed region, max over ranks
     stitch = None
-    if world > 1 and not replicas:
-        from paper_2304_13398_b200 import shard as _shard
-        lo, hi = plan["own"]
-        torch.distributed.barrier()
-        torch.cuda.synchronize(dev)
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        stitched = _shard.gls_window_stitch(ctx, lo, hi, dev)
-        s1.record(stream)
-        torch.cuda.synchronize(dev)
-        st_ms = s0.elapsed_time(s1)
-        tt = torch.tensor([st_ms], dtype=torch.float64, device=dev)
-        allv = [torch.zeros_like(tt) for _ in range(world)]
-        torch.distributed.all_gather(allv, tt)
-        stitch = {"ms": float(torch.stack(allv).max()), "nets": int(stitched.numel()),
-                  "bytes_per_rank": int(16 * stitched.numel()),
-                  "what": "full-run per-net checksums from the time windows (all_gather of counts and "
-                          "position-keyed terms over NCCL)"}
-        del stitched
+    try:
+        stitch = post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_hashes, stims)
+    except Exception as e:                      # the measured line must still be printed
+        log(f"stitch failed: {e!r}")
+        stitch = {"error": repr(e)}
 
     # e2e through the public API with host buffers (pinned), every step:
     # H2D of the given waveforms, simulate, D2H of the per-net hashes
@@ -356,6 +429,26 @@ def run_gls(a):
                       (f", first {len(e_sets)} of the rank's {len(stims)} stimulus sets" if len(stims) > 1 else "")}
         del pinned
 
+    # a10 at full size: the canonical CSR of the whole result through the public host API
+    # (device gather in net order, batch by batch through a staging buffer, one D2H each),
+    # timed once on rank 0 when it fits comfortably in host memory
+    readback = None
+    if rank == 0 and not a.no_e2e:
+        import psutil
+        rb_total = int(ctx.gls_get_net_counts().sum())
+        need = 8 * rb_total
+        avail = psutil.virtual_memory().available
+        if need < 0.4 * avail:
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            w = ctx.gls_get_waveforms()
+            dt = time.perf_counter() - t0
+            readback = {"ms": 1e3 * dt, "bytes": need, "gbs": need / dt / 1e9, "transitions": rb_total,
+                        "api": "gls_get_waveforms (host, pageable numpy buffer)"}
+            del w
+        else:
+            readback = {"skipped": f"{need / 1e9:.0f} GB result > 40 % of the host's available memory"}
+
     if len(stims) > 1:          # the parity check below is on the first set: simulate it again
         ctx.gls_set_input_waveforms_device(nl.num_inputs, stims[0][0].data_ptr(), stims[0][1].data_ptr(), stims[0][2])
         ctx.gls_simulate(duration)
@@ -367,7 +460,8 @@ def run_gls(a):
         r, dt, tmax = oracle_sample(nl, spec, cyc)
         cpu = {"value": r.gate_evals / dt, "unit": "gate-evals/s", "cores": 1, "kind": "oracle",
                "sample": f"{cfg} netlist ({nl.num_gates} gates), first {cyc} of {nc} clock cycles "
-                         f"(t <= {tmax} ps): {r.gate_evals} gate-evals in {dt:.2f} s, single thread"}
+                         f"(t <= {tmax} ps): {r.gate_evals} gate-evals in {dt:.2f} s, single thread",
+               **host_cpu()}
         gh = ctx.gls_get_net_hashes_window(0, tmax)
         mism = int((gh != r.hashes).sum())
         parity = {"window_ps": [0, tmax], "nets": int(gh.size), "hash_mismatches": mism,
@@ -402,7 +496,7 @@ def run_gls(a):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "gls::sim_kernel", "kernel_ms": kms, "alg_bytes_per_launch": alg},
-            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "stitch": stitch,
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "stitch": stitch, "readback": readback,
             # per step: init_given_kernel + sim_kernel (gls_simulate) and fanin_reads_kernel
             # (gls_get_stats' algorithmic-bytes count, read after every step for kernel_ms)
             # (C5: + validate_kernel of gls_set_input_waveforms_device per set)

@@ -155,6 +155,8 @@ int gls_set_config(gls_ctx *ctx, const gls_config *cfg);
  *                                    [1] in-edge RISE, output -> 1
  *                                    [2] in-edge FALL, output -> 0
  *                                    [3] in-edge FALL, output -> 1
+ *                                    (GLS_DELAY_INF: the pin has no relation to
+ *                                    the output, reading R9)
  *                                    (the paper's 5-D matrix Delay[cell][in][out]
  *                                    [edge][value], for single-output
  *                                    gates; output -> X uses min of the two,
@@ -166,6 +168,41 @@ int gls_set_config(gls_ctx *ctx, const gls_config *cfg);
 int gls_load_netlist(gls_ctx *ctx, int32_t num_inputs, int32_t num_gates,
                      const uint8_t *gate_type, const int64_t *fanin_offsets,
                      const int32_t *fanin_net, const uint32_t *pin_delay);
+
+/* ---- multi-output cells and UDPs (NEXT-2: §3.2 Delay P:329-333, §3.3 Module
+ * Function P:335-339) ---------------------------------------------------- */
+#define GLS_DELAY_INF 0xFFFFFFFFu  /* "no relation" between an input and an output pin
+                                      (P:331-333): the pin never enters the delay minimum;
+                                      an output change whose changed inputs are all
+                                      unrelated is not scheduled (reading R9)          */
+/* A standard cell template / UDP: a DAG of basic gates over the cell's inputs (the
+ * paper composes every cell function from the basic gates' functions), its
+ * outputs some of the DAG's nodes, evaluated with zero internal delay.  Node ids:
+ * 0..num_inputs-1 the cell inputs, num_inputs + j basic gate j (fan-in nodes < j's own). */
+typedef struct gls_cell_template {
+    int32_t num_inputs;              /* 1..4                                          */
+    int32_t num_outputs;             /* 1..8                                          */
+    int32_t num_gates;               /* 0..64                                         */
+    const uint8_t *gate_type;        /* [num_gates] GLS_BUF..GLS_MUX2                  */
+    const int32_t *gate_fanin_offsets; /* [num_gates + 1] into gate_fanin            */
+    const int32_t *gate_fanin;       /* node ids                                      */
+    const int32_t *output_node;      /* [num_outputs]                                 */
+} gls_cell_template;
+/* Load a netlist of cells (replaces any netlist; clears inputs and results).  Nets:
+ * 0..num_inputs-1 given, then the outputs of every cell in cell order (cell c's output
+ * q is net num_inputs + (outputs of the cells before c) + q).
+ *   cell_template [num_cells]      template id of each cell
+ *   cell_fanin    [Σ num_inputs]   driving net of each input pin, cells concatenated
+ *   cell_delay    [Σ num_inputs*num_outputs*4]  per cell Delay[in][out][edge][value],
+ *                                  edge RISE = 0 / FALL = 1, value 0 / 1 (the paper's 5-D
+ *                                  matrix), ps < 2^31 or GLS_DELAY_INF
+ * A gate-eval counts per cell OUTPUT.  Distinct output functions that are not a basic
+ * gate's share a (kLutCap - 3060 = 1036)-byte table area in shared memory (e.g. 4
+ * four-input or 16 three-input functions); more -> GLS_EINVAL.  Errors: GLS_EINVAL,
+ * GLS_ECYCLE, GLS_ENOMEM, GLS_ECUDA. */
+int gls_load_cells(gls_ctx *ctx, int32_t num_inputs, int32_t num_templates, const gls_cell_template *templates,
+                   int32_t num_cells, const int32_t *cell_template, const int32_t *cell_fanin,
+                   const uint32_t *cell_delay);
 
 /* ---- given waveforms (a2) ------------------------------------------------ */
 /* CSR of packed transitions on the num_inputs given nets (HOST pointers):

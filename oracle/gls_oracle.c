@@ -220,6 +220,103 @@ static int process_cell(int type, int k, const wave_t *const *in, const uint32_t
 }
 
 /* ---------------------------------------------------------------------------
+ * Multi-output cells (§3.2 Delay P:329-333, §3.3 Module Function P:335-339).
+ *
+ * A cell template is a small DAG of basic gates over the cell's input pins (the
+ * paper's standard cell template / UDP: "implement the logic functions of all basic
+ * logic gates and combine them according to the requirement of any standard cell
+ * template"); its outputs are some of the DAG's nodes, evaluated with zero
+ * internal delay.  Node ids: 0..n_in-1 the cell inputs, n_in + j basic gate j (its
+ * fan-in nodes < n_in + j).  Delays: the 5-D matrix Delay[cell][in][out][edge][value]
+ * (P:331), one [n_in][n_out][2][2] block per cell instance; DELAY_INF = "no relation"
+ * (P:331-333): such pins do not enter the minimum, and an output change whose changed
+ * pins are all unrelated is not scheduled (reading R9: literal Alg. 2 — the evaluation
+ * still advances, "currentSignals = newSignals").
+ * ------------------------------------------------------------------------- */
+#define DELAY_INF 0xFFFFFFFFu
+enum { CELL_MAX_IN = 4, CELL_MAX_OUT = 8, CELL_MAX_GATES = 64 };
+
+typedef struct {
+    int32_t n_in, n_out, n_gates;
+    const uint8_t *gate_type;      /* [n_gates] */
+    const int32_t *gate_fanin_off; /* [n_gates + 1] */
+    const int32_t *gate_fanin;     /* node ids */
+    const int32_t *output_node;    /* [n_out] */
+} oracle_template_t;
+
+/* the template's outputs for input values v[0..n_in-1] (Table 1 per basic gate) */
+static void eval_template(const oracle_template_t *t, const uint8_t *v, uint8_t *o)
+{
+    uint8_t node[CELL_MAX_IN + CELL_MAX_GATES];
+    for (int i = 0; i < t->n_in; i++) node[i] = v[i];
+    for (int j = 0; j < t->n_gates; j++) {
+        uint8_t x[4];
+        int k = t->gate_fanin_off[j + 1] - t->gate_fanin_off[j];
+        for (int q = 0; q < k; q++) x[q] = node[t->gate_fanin[t->gate_fanin_off[j] + q]];
+        node[t->n_in + j] = eval_gate(t->gate_type[j], x, k);
+    }
+    for (int q = 0; q < t->n_out; q++) o[q] = norm_z(node[t->output_node[q]]);
+}
+
+/* Algorithm 2 for one cell: all its outputs from one sweep of its inputs.
+ *   d[((i * n_out + q) * 2 + e) * 2 + o] = Delay[i][q][e][o]  (DELAY_INF: no relation) */
+static int process_multi(const oracle_template_t *t, const wave_t *const *in, const uint32_t *d,
+                         int64_t duration, wave_t *const *out, ostats_t *st)
+{
+    const int k = t->n_in, m = t->n_out;
+    uint8_t cur[CELL_MAX_IN];
+    int edge[CELL_MAX_IN];
+    int64_t idx[CELL_MAX_IN];
+    uint8_t out_sig[CELL_MAX_OUT], o[CELL_MAX_OUT];
+    for (int i = 0; i < k; i++) { cur[i] = VX; idx[i] = 0; }
+    for (int q = 0; q < m; q++) out_sig[q] = VX;
+    const int64_t INF = INT64_MAX;
+    for (;;) {
+        int64_t te = INF;
+        for (int i = 0; i < k; i++)
+            if (idx[i] < in[i]->n && in[i]->t[idx[i]] < te) te = in[i]->t[idx[i]];
+        if (te == INF) break;
+        st->gate_evals += m;               /* one calculateSignals per output */
+        int changed[CELL_MAX_IN] = {0, 0, 0, 0};
+        for (int i = 0; i < k; i++) {
+            if (idx[i] < in[i]->n && in[i]->t[idx[i]] == te) {
+                uint8_t nv = in[i]->v[idx[i]];
+                uint8_t a = norm_z(cur[i]), b = norm_z(nv);
+                if (a != b) {
+                    changed[i] = 1;
+                    edge[i] = rank01x(b) > rank01x(a) ? RISE : FALL;
+                }
+                cur[i] = nv;
+                idx[i]++;
+            }
+        }
+        eval_template(t, cur, o);
+        for (int q = 0; q < m; q++) {
+            if (o[q] != out_sig[q]) {                  /* P:473, reading R4a */
+                st->events++;
+                int64_t del = INF;                      /* min over related changed pins */
+                for (int i = 0; i < k; i++) {
+                    if (!changed[i]) continue;
+                    const uint32_t *di = d + ((i * m + q) * 2 + edge[i]) * 2;
+                    uint32_t x = (o[q] == VX) ? (di[0] < di[1] ? di[0] : di[1]) : di[o[q]];
+                    if (x != DELAY_INF && (int64_t)x < del) del = x;
+                }
+                if (del != INF) {                       /* reading R9: unrelated -> not scheduled */
+                    int rc = add_signal_change(out[q], te + del, o[q]);
+                    if (rc) return rc;
+                }
+            }
+            out_sig[q] = o[q];
+        }
+    }
+    for (int q = 0; q < m; q++) {
+        while (out[q]->n > 0 && out[q]->t[out[q]->n - 1] > duration) out[q]->n--;   /* reading R7 */
+        st->out_trans += out[q]->n;
+    }
+    return OR_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * Whole netlist: §2.1 objective.  Nets 0..P-1 are the given
  * waveforms (primary / pseudo-primary inputs); net P+g is the output of gate
  * g.  Gates are processed once all their input waveforms are known (Alg. 1's
@@ -338,6 +435,103 @@ int oracle_simulate(int32_t P, int32_t G, const uint8_t *type, const int64_t *fa
     }
     if (rc == OR_OK && qt != G) rc = OR_ECYCLE; /* combinational loop */
     free(pending); free(cons_off); free(cons); free(queue);
+    if (rc) { oracle_free(r); return rc; }
+    *out = r;
+    return OR_OK;
+}
+
+/* Cell netlist: nets 0..P-1 given; the outputs of cell c are nets P + first[c] + q
+ * (first[c] = outputs of the cells before c).  Cells in Kahn order as above. */
+int oracle_simulate_cells(int32_t P, int32_t T, const int32_t *tpl_nin, const int32_t *tpl_nout,
+                          const int32_t *tpl_ngates, const int32_t *tpl_gate_off, const uint8_t *tpl_gate_type,
+                          const int32_t *tpl_fanin_off, const int32_t *tpl_fanin, const int32_t *tpl_out_off,
+                          const int32_t *tpl_out_node, int32_t C, const int32_t *cell_tpl,
+                          const int32_t *cell_fanin, const uint32_t *cell_delay, const int64_t *in_off,
+                          const uint64_t *in_trans, int64_t duration, oracle_result_t **out)
+{
+    *out = NULL;
+    if (P < 0 || T < 0 || C < 0 || duration < 0) return OR_EINVAL;
+    oracle_template_t *tp = (oracle_template_t *)calloc((size_t)(T ? T : 1), sizeof(oracle_template_t));
+    if (!tp) return OR_ENOMEM;
+    for (int32_t i = 0; i < T; i++) {
+        tp[i].n_in = tpl_nin[i];
+        tp[i].n_out = tpl_nout[i];
+        tp[i].n_gates = tpl_ngates[i];
+        tp[i].gate_type = tpl_gate_type + tpl_gate_off[i];
+        tp[i].gate_fanin_off = tpl_fanin_off + tpl_gate_off[i] + i;   /* n_gates + 1 entries each */
+        tp[i].gate_fanin = tpl_fanin;
+        tp[i].output_node = tpl_out_node + tpl_out_off[i];
+        if (tp[i].n_in < 1 || tp[i].n_in > CELL_MAX_IN || tp[i].n_out < 1 || tp[i].n_out > CELL_MAX_OUT ||
+            tp[i].n_gates < 0 || tp[i].n_gates > CELL_MAX_GATES) { free(tp); return OR_EINVAL; }
+    }
+    int64_t *first = (int64_t *)calloc((size_t)C + 1, sizeof(int64_t));
+    int64_t *pin0 = (int64_t *)calloc((size_t)C + 1, sizeof(int64_t));
+    int64_t *dly0 = (int64_t *)calloc((size_t)C + 1, sizeof(int64_t));
+    if (!first || !pin0 || !dly0) { free(tp); free(first); free(pin0); free(dly0); return OR_ENOMEM; }
+    for (int32_t c = 0; c < C; c++) {
+        if (cell_tpl[c] < 0 || cell_tpl[c] >= T) { free(tp); free(first); free(pin0); free(dly0); return OR_EINVAL; }
+        const oracle_template_t *t = &tp[cell_tpl[c]];
+        first[c + 1] = first[c] + t->n_out;
+        pin0[c + 1] = pin0[c] + t->n_in;
+        dly0[c + 1] = dly0[c] + (int64_t)t->n_in * t->n_out * 4;
+    }
+    const int64_t G = first[C], N = (int64_t)P + G;
+    oracle_result_t *r = (oracle_result_t *)calloc(1, sizeof(*r));
+    int64_t *pending = (int64_t *)calloc((size_t)(C ? C : 1), sizeof(int64_t));
+    int64_t *cons_off = (int64_t *)calloc((size_t)N + 1, sizeof(int64_t));
+    int32_t *cons = (int32_t *)malloc((size_t)(pin0[C] ? pin0[C] : 1) * sizeof(int32_t));
+    int32_t *queue = (int32_t *)malloc((size_t)(C ? C : 1) * sizeof(int32_t));
+    int32_t *owner = (int32_t *)malloc((size_t)(G ? G : 1) * sizeof(int32_t));
+    int rc = OR_OK;
+    if (!r || !pending || !cons_off || !cons || !queue || !owner) rc = OR_ENOMEM;
+    if (!rc) {
+        r->P = P;
+        r->G = (int32_t)G;
+        r->w = (wave_t *)calloc((size_t)(N ? N : 1), sizeof(wave_t));
+        if (!r->w) rc = OR_ENOMEM;
+    }
+    for (int32_t p = 0; !rc && p < P; p++)
+        for (int64_t j = in_off[p]; j < in_off[p + 1] && !rc; j++)
+            rc = wave_push(&r->w[p], (int64_t)(in_trans[j] >> 2), (uint8_t)(in_trans[j] & 3));
+    for (int32_t c = 0; !rc && c < C; c++) {
+        for (int64_t q = first[c]; q < first[c + 1]; q++) owner[q] = c;
+        for (int64_t e = pin0[c]; e < pin0[c + 1]; e++) {
+            if (cell_fanin[e] < 0 || cell_fanin[e] >= N) { rc = OR_EINVAL; break; }
+            cons_off[cell_fanin[e] + 1]++;
+            if (cell_fanin[e] >= P) pending[c]++;
+        }
+    }
+    if (!rc) {
+        for (int64_t n = 0; n < N; n++) cons_off[n + 1] += cons_off[n];
+        int64_t *fill = (int64_t *)malloc((size_t)(N ? N : 1) * sizeof(int64_t));
+        if (!fill) rc = OR_ENOMEM;
+        else {
+            memcpy(fill, cons_off, (size_t)N * sizeof(int64_t));
+            for (int32_t c = 0; c < C; c++)
+                for (int64_t e = pin0[c]; e < pin0[c + 1]; e++) cons[fill[cell_fanin[e]]++] = c;
+            free(fill);
+        }
+    }
+    int64_t qh = 0, qt = 0;
+    for (int32_t c = 0; !rc && c < C; c++)
+        if (pending[c] == 0) queue[qt++] = c;
+    while (!rc && qh < qt) {
+        int32_t c = queue[qh++];
+        const oracle_template_t *t = &tp[cell_tpl[c]];
+        const wave_t *in[CELL_MAX_IN];
+        wave_t *outs[CELL_MAX_OUT];
+        for (int i = 0; i < t->n_in; i++) in[i] = &r->w[cell_fanin[pin0[c] + i]];
+        for (int q = 0; q < t->n_out; q++) outs[q] = &r->w[P + first[c] + q];
+        rc = process_multi(t, in, cell_delay + dly0[c], duration, outs, &r->st);
+        /* the cell's outputs are known: unlock the consumers (once per consuming pin) */
+        for (int q = 0; !rc && q < t->n_out; q++) {
+            int64_t n = (int64_t)P + first[c] + q;
+            for (int64_t e = cons_off[n]; e < cons_off[n + 1]; e++)
+                if (--pending[cons[e]] == 0) queue[qt++] = cons[e];
+        }
+    }
+    if (!rc && qt != C) rc = OR_ECYCLE;
+    free(tp); free(first); free(pin0); free(dly0); free(pending); free(cons_off); free(cons); free(queue); free(owner);
     if (rc) { oracle_free(r); return rc; }
     *out = r;
     return OR_OK;

@@ -74,7 +74,7 @@ bool arity_ok(int type, int64_t k) {
 const std::vector<uint8_t>& lut_table() {
     static std::vector<uint8_t> t;
     if (t.empty()) {
-        t.assign(kLutBytes, 2);
+        t.assign(kLutCap, 2);                     // (the rest: cell output functions, gls_load_cells)
         for (int type = 0; type < kNumTypes; ++type)
             for (int k = 1; k <= 4; ++k) {
                 int base = lut_offset(type, k);
@@ -127,6 +127,7 @@ struct gls_ctx {
     int32_t P = 0, G = 0, L = 0;
     int64_t E = 0;
     int64_t halo = 1;
+    bool has_inf = false;                   // some pin delay is GLS_DELAY_INF
     std::vector<uint32_t> perm;        // internal gate -> user gate
     std::vector<uint32_t> inv;         // user gate -> internal gate
     std::vector<int64_t> net_fanout;   // internal net -> pins it drives
@@ -166,6 +167,7 @@ struct gls_ctx {
     DevBuf<uint8_t> d_ck_vb;
     DevBuf<uint64_t> d_deep;
     DevBuf<uint64_t> d_wscr;
+    DevBuf<unsigned char> d_waux;
     DevBuf<uint64_t> d_hash;                // result checksums (kept: no malloc/free per readback)
     DevBuf<Ctl> d_ctl;
     DevBuf<unsigned> d_flag;
@@ -239,6 +241,7 @@ SimParams params(gls_ctx* ctx) {
     p.work = ctx->d_work.p;
     p.deep = ctx->d_deep.p;
     p.wscr = ctx->d_wscr.p;
+    p.waux = ctx->d_waux.p;
     p.deep_wtop = ctx->d_deep_wtop.p;
     p.fo_off = ctx->d_fo_off.p;
     p.fo_gate = ctx->d_fo_gate.p;
@@ -389,9 +392,9 @@ int gls_create(gls_ctx** out, int cuda_device, void* cuda_stream) {
     if (e == cudaSuccess) e = ctx->d_ctl.alloc(1);
     if (e == cudaSuccess) e = ctx->d_flag.alloc(4);
     if (e == cudaSuccess) e = ctx->d_flag64.alloc(4);
-    if (e == cudaSuccess) e = ctx->d_lut.alloc(kLutBytes);
+    if (e == cudaSuccess) e = ctx->d_lut.alloc(kLutCap);
     if (e == cudaSuccess)
-        e = cudaMemcpy(ctx->d_lut.p, lut_table().data(), kLutBytes, cudaMemcpyHostToDevice);
+        e = cudaMemcpy(ctx->d_lut.p, lut_table().data(), kLutCap, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaGetLastError();
         delete ctx;
@@ -420,26 +423,15 @@ int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
     return GLS_OK;
 }
 
-int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, const int64_t* off,
-                     const int32_t* net, const uint32_t* delay) {
-    if (!ctx) return GLS_EINVAL;
-    if (P < 0 || G < 0 || (int64_t)P + G >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "bad net counts");
-    if (G > 0 && (!type || !off)) return fail(ctx, GLS_EINVAL, "null netlist array");
+}  // extern "C"
+
+// a1 for gates given by arity, LUT base and pin delays (basic gates or expanded cell
+// outputs): Kahn order, levels, the fan-in CSR in level order, fan-out lists, halo;
+// upload (with the LUT table `lut`, kLutCap bytes).
+static int load_gates(gls_ctx* ctx, int32_t P, int32_t G, const uint16_t* lb, const int64_t* off, const int32_t* net,
+                      const uint32_t* delay, const std::vector<uint8_t>& lut) {
     const int64_t N = (int64_t)P + G;
     const int64_t E = G > 0 ? off[G] : 0;
-    if (G > 0 && off[0] != 0) return fail(ctx, GLS_EINVAL, "fanin_offsets[0] != 0");
-    if (E < 0 || E >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "pin count out of range");
-    if (E > 0 && (!net || !delay)) return fail(ctx, GLS_EINVAL, "null pin array");
-    for (int32_t g = 0; g < G; ++g) {
-        int64_t k = off[g + 1] - off[g];
-        if (type[g] >= kNumTypes) return fail(ctx, GLS_EINVAL, "gate %d: unknown type %d", g, (int)type[g]);
-        if (!arity_ok(type[g], k)) return fail(ctx, GLS_EINVAL, "gate %d: arity %lld invalid", g, (long long)k);
-        for (int64_t e = off[g]; e < off[g + 1]; ++e) {
-            if (net[e] < 0 || net[e] >= N) return fail(ctx, GLS_EINVAL, "gate %d: net id %d out of range", g, net[e]);
-            for (int q = 0; q < 4; ++q)
-                if (delay[4 * e + q] >= (1u << 31)) return fail(ctx, GLS_EINVAL, "pin %lld: delay >= 2^31", (long long)e);
-        }
-    }
     // Kahn topological order; level(g) = 1 + max level of driving gates (PIs at 0)
     std::vector<int32_t> indeg(G, 0), level(G, 0), order;
     std::vector<int64_t> fo_off((size_t)G + 1, 0);
@@ -494,8 +486,8 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
         int k = (int)(off[g + 1] - off[g]);
         ginfo[i].pin_off = pin;
         ginfo[i].k = (uint8_t)k;
-        ginfo[i].lut_base = (uint16_t)lut_offset(type[g], k);
-        ginfo[i].pad = 0;
+        ginfo[i].lut_base = lb[g];
+        ginfo[i].flags = 0;
         uint32_t dmax = 0;
         int64_t a = 0;
         for (int q = 0; q < k; ++q) {
@@ -504,7 +496,10 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
             uint32_t si = s < P ? (uint32_t)s : (uint32_t)(P + inv[s - P]);
             psrc[pin] = si;
             pdel[pin] = make_uint4(delay[4 * e], delay[4 * e + 1], delay[4 * e + 2], delay[4 * e + 3]);
-            dmax = std::max({dmax, delay[4 * e], delay[4 * e + 1], delay[4 * e + 2], delay[4 * e + 3]});
+            for (int d = 0; d < 4; ++d) {
+                if (delay[4 * e + d] != kDelayInf) dmax = std::max(dmax, delay[4 * e + d]);   // halo: finite delays
+                else ginfo[i].flags |= kGateInf;
+            }
             ++fanout[si];
             a = std::max(a, arrive[si]);
             ++pin;
@@ -568,11 +563,151 @@ int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, co
     ctx->L = L;
     ctx->E = E;
     ctx->halo = maxA + 1;
+    ctx->has_inf = false;
+    for (int32_t i = 0; i < G; ++i) ctx->has_inf = ctx->has_inf || (ginfo[i].flags & kGateInf);
     ctx->perm.swap(perm);
     ctx->inv.swap(inv);
     ctx->net_fanout.swap(fanout);
+    CK(cudaMemcpy(ctx->d_lut.p, lut.data(), kLutCap, cudaMemcpyHostToDevice));
     ctx->has_netlist = true;
     return GLS_OK;
+}
+
+
+extern "C" {
+
+int gls_load_netlist(gls_ctx* ctx, int32_t P, int32_t G, const uint8_t* type, const int64_t* off,
+                     const int32_t* net, const uint32_t* delay) {
+    if (!ctx) return GLS_EINVAL;
+    if (P < 0 || G < 0 || (int64_t)P + G >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "bad net counts");
+    if (G > 0 && (!type || !off)) return fail(ctx, GLS_EINVAL, "null netlist array");
+    const int64_t N = (int64_t)P + G;
+    const int64_t E = G > 0 ? off[G] : 0;
+    if (G > 0 && off[0] != 0) return fail(ctx, GLS_EINVAL, "fanin_offsets[0] != 0");
+    if (E < 0 || E >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "pin count out of range");
+    if (E > 0 && (!net || !delay)) return fail(ctx, GLS_EINVAL, "null pin array");
+    for (int32_t g = 0; g < G; ++g) {
+        int64_t k = off[g + 1] - off[g];
+        if (type[g] >= kNumTypes) return fail(ctx, GLS_EINVAL, "gate %d: unknown type %d", g, (int)type[g]);
+        if (!arity_ok(type[g], k)) return fail(ctx, GLS_EINVAL, "gate %d: arity %lld invalid", g, (long long)k);
+        for (int64_t e = off[g]; e < off[g + 1]; ++e) {
+            if (net[e] < 0 || net[e] >= N) return fail(ctx, GLS_EINVAL, "gate %d: net id %d out of range", g, net[e]);
+            for (int q = 0; q < 4; ++q)
+                if (delay[4 * e + q] >= (1u << 31) && delay[4 * e + q] != kDelayInf)
+                    return fail(ctx, GLS_EINVAL, "pin %lld: delay >= 2^31 (and not GLS_DELAY_INF)", (long long)e);
+        }
+    }
+    std::vector<uint16_t> lb((size_t)std::max<int32_t>(G, 1));
+    for (int32_t g = 0; g < G; ++g) lb[g] = (uint16_t)lut_offset(type[g], (int)(off[g + 1] - off[g]));
+    return load_gates(ctx, P, G, lb.data(), off, net, delay, lut_table());
+}
+
+// Multi-output cells (§3.2 Delay P:329-333, §3.3 Module Function P:335-339): every
+// template output is a function of the cell's inputs composed of basic gates (the
+// library's own dual-rail evaluation, lut_eval), tabulated once per distinct function
+// (a basic gate's table when it is one, else a table in the cell area of the LUT); each
+// cell output becomes a gate with the cell's input pins and its own slice of the 5-D
+// delay matrix (GLS_DELAY_INF: no relation, reading R9).
+int gls_load_cells(gls_ctx* ctx, int32_t P, int32_t T, const gls_cell_template* tpl, int32_t C,
+                   const int32_t* cell_tpl, const int32_t* cell_fanin, const uint32_t* cell_delay) {
+    if (!ctx) return GLS_EINVAL;
+    if (P < 0 || T < 0 || C < 0) return fail(ctx, GLS_EINVAL, "bad counts");
+    if ((T > 0 && !tpl) || (C > 0 && (!cell_tpl || !cell_fanin || !cell_delay)))
+        return fail(ctx, GLS_EINVAL, "null cell array");
+    std::vector<uint8_t> lut = lut_table();
+    int used = kLutBytes;
+    std::vector<std::vector<uint16_t>> out_lb((size_t)T);
+    for (int32_t i = 0; i < T; ++i) {
+        const gls_cell_template& t = tpl[i];
+        if (t.num_inputs < 1 || t.num_inputs > 4 || t.num_outputs < 1 || t.num_outputs > 8 || t.num_gates < 0 ||
+            t.num_gates > 64 || (t.num_gates > 0 && (!t.gate_type || !t.gate_fanin_offsets || !t.gate_fanin)) ||
+            !t.output_node)
+            return fail(ctx, GLS_EINVAL, "template %d: bad shape", i);
+        for (int j = 0; j < t.num_gates; ++j) {
+            const int64_t k = t.gate_fanin_offsets[j + 1] - t.gate_fanin_offsets[j];
+            if (t.gate_type[j] >= kNumTypes || !arity_ok(t.gate_type[j], k))
+                return fail(ctx, GLS_EINVAL, "template %d gate %d: type / arity", i, j);
+            for (int64_t q = t.gate_fanin_offsets[j]; q < t.gate_fanin_offsets[j + 1]; ++q)
+                if (t.gate_fanin[q] < 0 || t.gate_fanin[q] >= t.num_inputs + j)
+                    return fail(ctx, GLS_EINVAL, "template %d gate %d: node %d (not an earlier node)", i, j, t.gate_fanin[q]);
+        }
+        for (int q = 0; q < t.num_outputs; ++q)
+            if (t.output_node[q] < 0 || t.output_node[q] >= t.num_inputs + t.num_gates)
+                return fail(ctx, GLS_EINVAL, "template %d output %d: node out of range", i, q);
+        const int k = t.num_inputs, n = 1 << (2 * k);
+        for (int q = 0; q < t.num_outputs; ++q) {
+            std::vector<uint8_t> tab((size_t)n, 2);
+            for (int idx = 0; idx < n; ++idx) {
+                int node[4 + 64];
+                bool valid = true;
+                for (int a = 0; a < k; ++a) {
+                    node[a] = (idx >> (2 * a)) & 3;
+                    if (node[a] == 3) valid = false;   // the kernel indexes normalised codes
+                }
+                if (!valid) continue;
+                for (int j = 0; j < t.num_gates; ++j) {
+                    int v[4];
+                    const int32_t f0 = t.gate_fanin_offsets[j];
+                    const int kk = (int)(t.gate_fanin_offsets[j + 1] - f0);
+                    for (int a = 0; a < kk; ++a) v[a] = node[t.gate_fanin[f0 + a]];
+                    node[k + j] = lut_eval(t.gate_type[j], kk, v);
+                }
+                const int o = node[t.output_node[q]];
+                tab[(size_t)idx] = (uint8_t)(o == 3 ? 2 : o);
+            }
+            // a basic gate's table, an earlier cell table, or a new one
+            int base = -1;
+            for (int ty = 0; ty < kNumTypes && base < 0; ++ty)
+                if (arity_ok(ty, k) && std::equal(tab.begin(), tab.end(), lut.begin() + lut_offset(ty, k)))
+                    base = lut_offset(ty, k);
+            for (int b0 = kLutBytes; base < 0 && b0 + n <= used; ++b0)
+                if (std::equal(tab.begin(), tab.end(), lut.begin() + b0)) base = b0;
+            if (base < 0) {
+                if (used + n > kLutCap)
+                    return fail(ctx, GLS_EINVAL, "cell output functions need more than the %d-byte LUT area", kLutCap - kLutBytes);
+                std::copy(tab.begin(), tab.end(), lut.begin() + used);
+                base = used;
+                used += n;
+            }
+            out_lb[(size_t)i].push_back((uint16_t)base);
+        }
+    }
+    // expand: cell c's output q is gate (first[c] + q), net P + first[c] + q
+    int64_t G = 0, pins = 0, dl = 0;
+    for (int32_t c = 0; c < C; ++c) {
+        if (cell_tpl[c] < 0 || cell_tpl[c] >= T) return fail(ctx, GLS_EINVAL, "cell %d: template id", c);
+        G += tpl[cell_tpl[c]].num_outputs;
+    }
+    if ((int64_t)P + G >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "bad net counts");
+    const int64_t N = (int64_t)P + G;
+    std::vector<uint16_t> lb((size_t)std::max<int64_t>(G, 1));
+    std::vector<int64_t> off((size_t)G + 1, 0);
+    std::vector<int32_t> net;
+    std::vector<uint32_t> delay;
+    int64_t g = 0;
+    for (int32_t c = 0; c < C; ++c) {
+        const gls_cell_template& t = tpl[cell_tpl[c]];
+        for (int a = 0; a < t.num_inputs; ++a)
+            if (cell_fanin[pins + a] < 0 || cell_fanin[pins + a] >= N)
+                return fail(ctx, GLS_EINVAL, "cell %d: net id %d out of range", c, cell_fanin[pins + a]);
+        for (int q = 0; q < t.num_outputs; ++q, ++g) {
+            lb[(size_t)g] = out_lb[(size_t)cell_tpl[c]][(size_t)q];
+            for (int a = 0; a < t.num_inputs; ++a) {
+                net.push_back(cell_fanin[pins + a]);
+                for (int e = 0; e < 4; ++e) {           // [in][out][edge][value] -> pin (rise0, rise1, fall0, fall1)
+                    const uint32_t d = cell_delay[dl + ((int64_t)a * t.num_outputs + q) * 4 + e];
+                    if (d >= (1u << 31) && d != kDelayInf)
+                        return fail(ctx, GLS_EINVAL, "cell %d: delay >= 2^31 (and not GLS_DELAY_INF)", c);
+                    delay.push_back(d);
+                }
+            }
+            off[(size_t)g + 1] = (int64_t)net.size();
+        }
+        pins += t.num_inputs;
+        dl += (int64_t)t.num_inputs * t.num_outputs * 4;
+    }
+    if ((int64_t)net.size() >= (1ll << 31)) return fail(ctx, GLS_EINVAL, "pin count out of range");
+    return load_gates(ctx, P, (int32_t)G, lb.data(), off.data(), net.data(), delay.data(), lut);
 }
 
 static int set_inputs_common(gls_ctx* ctx, int32_t P, int64_t total) {
@@ -704,6 +839,9 @@ int gls_simulate_window(gls_ctx* ctx, int64_t t_begin, int64_t t_end, int64_t du
     if (rc) return rc;
     if (t_begin < 0 || t_end < t_begin) return fail(ctx, GLS_EINVAL, "window [%lld, %lld) invalid",
                                                     (long long)t_begin, (long long)t_end);
+    if (ctx->has_inf && t_begin > 0)
+        return fail(ctx, GLS_EINVAL, "time windows need finite delays: with GLS_DELAY_INF an output keeps a value "
+                                     "from before any halo (reading R9)");
     cudaSetDevice(ctx->device);
     ctx->has_result = false;
     ctx->window_active = false;
@@ -748,6 +886,7 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
     int blocks = ctx->cfg.blocks_per_sm > 0 ? std::min(maxb, ctx->cfg.blocks_per_sm * sms) : maxb;
     if (blocks < 1) return fail(ctx, GLS_ECUDA, "simulation kernel cannot be resident (occupancy 0)");
     if (ctx->d_wscr.n < warp_scratch_entries(blocks)) CK(ctx->d_wscr.alloc(warp_scratch_entries(blocks)));
+    if (ctx->d_waux.n < warp_aux_bytes(blocks)) CK(ctx->d_waux.alloc(warp_aux_bytes(blocks)));
     const int64_t nwarps = (int64_t)blocks * (kThreads / 32);
     if (ctx->deep_per_warp == 0) ctx->deep_per_warp = ctx->cfg.deep_per_warp > 0 ? ctx->cfg.deep_per_warp : (1 << 16);
     if ((int64_t)ctx->d_deep.n != nwarps * ctx->deep_per_warp) CK(ctx->d_deep.alloc(nwarps * ctx->deep_per_warp));

@@ -18,7 +18,10 @@ namespace gls {
 
 constexpr int kNumTypes = 9;
 constexpr int kLutPerType = 4 + 16 + 64 + 256;       // arity 1..4, index = packed 2-bit codes
-constexpr int kLutBytes = kLutPerType * kNumTypes;   // 3060 B, staged in shared memory
+constexpr int kLutBytes = kLutPerType * kNumTypes;   // 3060 B: the basic gates' tables
+constexpr int kLutCap = 4096;                        // smem LUT: basic tables + cell output functions (a3)
+constexpr uint32_t kDelayInf = 0xFFFFFFFFu;          // "no relation" (reading R9)
+constexpr uint32_t kDelayInf16 = 0xFFFFu;            // the same in the u16 delay table of the 32-bit sweep
 constexpr uint64_t kInfEntry = ~0ull;                // head of an exhausted cursor
 constexpr int kRing = 32;                            // on-chip pending-schedule ring (power of 2)
 #ifndef GLS_THREADS
@@ -35,9 +38,10 @@ struct GateInfo {
     uint32_t pin_off;   // first pin in pin_src / pin_delay
     uint16_t lut_base;  // lut_offset(type, arity)
     uint8_t k;          // arity 1..4
-    uint8_t pad;
+    uint8_t flags;      // kGateInf: a pin delay is GLS_DELAY_INF (never time-chunked, see kernels)
 };
 
+constexpr uint8_t kGateInf = 1;
 enum : unsigned { kErrArena = 1u, kErrChunks = 2u, kErrDeep = 4u, kErrInput = 8u, kErrBug = 16u, kErrWatchdog = 32u };
 
 // device control block, initialised by the host before each run
@@ -73,7 +77,7 @@ struct SimParams {
     const GateInfo* gate;       // [G]
     const uint32_t* pin_src;    // [E] internal net id of each pin's driver
     const uint4* pin_delay;     // [E] (rise->0, rise->1, fall->0, fall->1)
-    const uint8_t* lut;         // [kLutBytes]
+    const uint8_t* lut;         // [kLutCap]
     uint64_t* arena;
     unsigned long long arena_cap;     // entries
     uint32_t* net_ck;           // [P+G] first chunk id
@@ -91,6 +95,7 @@ struct SimParams {
     unsigned long long* work;   // [L+1] per-level work counters
     uint64_t* deep;             // deep-backtrace scratch: one region per warp
     uint64_t* wscr;             // per-warp output scratch
+    void* waux;                 // per-warp auxiliary unit fields (engine 0)
     unsigned long long deep_cap;
     unsigned long long deep_per_warp;
     unsigned long long* deep_wtop;  // [warps] bump pointer of each warp's region
@@ -110,6 +115,7 @@ struct SimParams {
 cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaStream_t s);
 cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s);
 size_t warp_scratch_entries(int blocks);
+size_t warp_aux_bytes(int blocks);
 int max_coresident_blocks(int device, int engine, int sched, int* per_sm);
 // time-window slice of the given waveforms (gls_simulate_window): per net the number of
 // kept entries, then the entries (collapse at t_clamp, keep t_clamp < t < t_end)

@@ -237,6 +237,7 @@ struct ChunkSetup {
     uint32_t src[4];
     uint4 d[4];
     uint32_t k, lut_base, dmin, dmax, pin_off;
+    bool inf;                   // some delay is GLS_DELAY_INF: the gate is one chunk (no halo starts)
     long long T0, T1, tau0;
 };
 
@@ -328,15 +329,17 @@ __device__ __noinline__ void run_chunk(const SimParams& p, const ChunkSetup& s, 
                     }
                 }
                 long long rr = t + (long long)del;               // o_k.t = t + del
-                // addSignalChange with Eq. 1: deny pending schedules at >= rr
-                while (hi != lo && etime(ring[(hi - 1) & mask]) >= rr) --hi;
-                uint32_t tv = hi != lo ? (uint32_t)(ring[(hi - 1) & mask] & 3u) : lastv;
-                if (tv != E) {
-                    if (hi - lo >= cap) {
-                        overflow = true;
-                    } else {
-                        ring[hi & mask] = ((uint64_t)rr << 2) | E;
-                        ++hi;
+                if (del != kDelayInf) {                          // reading R9: unrelated pins -> no schedule
+                    // addSignalChange with Eq. 1: deny pending schedules at >= rr
+                    while (hi != lo && etime(ring[(hi - 1) & mask]) >= rr) --hi;
+                    uint32_t tv = hi != lo ? (uint32_t)(ring[(hi - 1) & mask] & 3u) : lastv;
+                    if (tv != E) {
+                        if (hi - lo >= cap) {
+                            overflow = true;
+                        } else {
+                            ring[hi & mask] = ((uint64_t)rr << 2) | E;
+                            ++hi;
+                        }
                     }
                 }
                 if (t >= T0) ++events;
@@ -408,6 +411,7 @@ __device__ void plan_level(const SimParams& p, int l, unsigned gwarp, unsigned n
             unsigned long long c = (n_in + (unsigned long long)p.M - 1) / (unsigned long long)p.M;
             if (c < 1) c = 1;
             if (c > lenref + 1) c = lenref + 1;
+            if (g.flags & kGateInf) c = 1;              // no halo starts with unrelated pins (reading R9)
             nch = (unsigned)c;
             p.gate_nin[gi] = n_in;
         }
@@ -473,8 +477,13 @@ __device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetu
             s.src[i] = src;
             uint4 d = p.pin_delay[g.pin_off + i];
             s.d[i] = d;
-            dmin = min(dmin, min(min(d.x, d.y), min(d.z, d.w)));
-            dmax = max(dmax, max(max(d.x, d.y), max(d.z, d.w)));
+            const uint32_t f[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)                   // finite delays only (GLS_DELAY_INF: no relation)
+                if (f[q] != kDelayInf) {
+                    dmin = min(dmin, f[q]);
+                    dmax = max(dmax, f[q]);
+                }
             unsigned long long len = __ldcg(&p.net_len[src]);
             n_in += len;
             if (len > lenref) { lenref = len; ref = src; }
@@ -483,8 +492,9 @@ __device__ void setup_chunk(const SimParams& p, unsigned long long id, ChunkSetu
             s.d[i] = make_uint4(0, 0, 0, 0);
         }
     }
-    s.dmin = dmin;
+    s.dmin = dmin == 0xffffffffu ? 0u : dmin;
     s.dmax = dmax;
+    s.inf = (g.flags & kGateInf) != 0;
     // chunk boundaries: quantiles of the longest fan-in's transition times
     auto qidx = [&](uint32_t cc) -> unsigned long long {
         unsigned long long q = lenref / nch, rm = lenref % nch;
@@ -661,6 +671,7 @@ __device__ void plan_gate(const SimParams& p, uint32_t c) {
     unsigned long long nch = (n_in + (unsigned long long)p.M - 1) / (unsigned long long)p.M;
     if (nch < 1) nch = 1;
     if (nch > lenref + 1) nch = lenref + 1;
+    if (g.flags & kGateInf) nch = 1;                    // no halo starts with unrelated pins (reading R9)
     unsigned long long base = 0;
     if (lane == 0) base = atomicAdd(&p.ctl->chunk_top, nch);
     base = __shfl_sync(0xffffffffu, base, 0);
@@ -777,7 +788,7 @@ namespace gls {
 template <int ENGINE, bool DATAFLOW>
 __global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(const __grid_constant__ SimParams p) {
     uint8_t* const s_lut = ln::g_lut;
-    for (int i = threadIdx.x; i < kLutBytes; i += blockDim.x) s_lut[i] = p.lut[i];
+    for (int i = threadIdx.x; i < kLutCap; i += blockDim.x) s_lut[i] = p.lut[i];
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const unsigned warps_per_block = blockDim.x >> 5;
@@ -1097,6 +1108,8 @@ static const void* kernel_for(int engine, int sched) {
     if (engine == 1) return (const void*)sim_kernel<1, false>;
     return sched == 1 ? (const void*)sim_kernel<0, false> : (const void*)sim_kernel<0, true>;
 }
+
+size_t warp_aux_bytes(int blocks) { return (size_t)blocks * (kThreads / 32) * sizeof(ln::WarpAux); }
 
 size_t warp_scratch_entries(int blocks) {
     return (size_t)blocks * (kThreads / 32) * ln::kScratchPerWarp;

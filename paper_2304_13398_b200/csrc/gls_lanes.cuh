@@ -39,7 +39,8 @@ namespace ln {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint32_t kRelInf = 0xffffffffu;
 constexpr uint32_t kRebaseQ = 0x80000000u;       // entry form of t - B = 2^29
-constexpr uint32_t kFastDelay = 1u << 16;        // gates with dmax below this use the 32-bit sweep (u16 delays)
+constexpr uint32_t kFastDelay = 0xFFFFu;         // gates with dmax below this use the 32-bit sweep (u16 delays;
+                                                 // 0xFFFF there = GLS_DELAY_INF)
 #ifndef GLS_LCAP
 #define GLS_LCAP 2048
 #endif
@@ -163,11 +164,11 @@ struct Batch {
     long long c_T0[MAXC];                  // chunk start time
     uint32_t c_total[MAXC];
     uint8_t c_first[MAXC], c_nsl[MAXC];    // first unit, static slices
+    uint8_t c_inf[MAXC];                   // the chunk's gate has a GLS_DELAY_INF pin: one unit, never split
     long long u_T0[MAXU], u_T1[MAXU];      // unit time range
     uint32_t u_soff[MAXU], u_cnt[MAXU];    // outputs: lane-scratch offset, count
     uint32_t u_pre[MAXU];                  // offset of the unit's outputs inside its chunk
     uint32_t u_est[MAXU];                  // expected merged entries
-    uint32_t u_deep[MAXU];                 // fallback: deep-ring offset in the warp's region (~0: none)
     uint8_t u_chunk[MAXU], u_slice[MAXU], u_lane[MAXU], u_vb[MAXU], u_st[MAXU], u_next[MAXU];
     int qhead;                             // next static unit to hand out
     int nun;                               // units (static + split)
@@ -175,17 +176,25 @@ struct Batch {
     uint32_t lev[32], levt[32];            // per-lane gate-evals / events of the batch
     uint8_t sv_it[32];                     // (set-up call: the lane's round iteration,
     uint16_t sv_used[32];                  //  scratch fill)
-    uint32_t u_sev[MAXU], u_sevt[MAXU];    // the lane's counts when the unit started
     int8_t u_lnext[MAXU];                  // next unit taken by the same lane (-1: last)
     int8_t lane_first[32], lane_last[32];  // the lane's units in the order it took them
 };
 constexpr size_t kBatchBytes = (sizeof(Batch) + 15) & ~(size_t)15;
+// rarely used per-unit fields in global memory (per warp), so that the shared Batch
+// leaves room for L1
+struct WarpAux {
+    uint32_t u_deep[MAXU];                 // fallback: deep-ring offset in the warp's region (~0: none)
+    uint32_t u_sev[MAXU], u_sevt[MAXU];    // the lane's counts when the unit started
+};
+__device__ __forceinline__ WarpAux& warp_aux(const SimParams& p) {
+    return reinterpret_cast<WarpAux*>(p.waux)[warp_global_id()];
+}
 
 // Shared memory of a CTA (namespace scope, so addresses are constants plus the thread
 // index, not registers): the 4-value LUT (a3, staged per CTA), then per-thread delay
 // tables (u16 [24][kThreads]), one Batch per warp, the per-thread pin cursor columns.
 constexpr int kDtabWords = 24;
-__shared__ uint8_t g_lut[kLutBytes];
+__shared__ uint8_t g_lut[kLutCap];
 extern __shared__ __align__(16) unsigned char g_dyn[];
 constexpr size_t kDynBytes = (size_t)kDtabWords * kThreads * 2 + kBatchBytes * (kThreads / 32) + kPinSmBytes;
 __device__ __forceinline__ Batch& warp_batch() {
@@ -217,12 +226,15 @@ __device__ __forceinline__ void fill_dtab(T* dtab, int dstride, const ChunkSetup
 #pragma unroll
     for (int i = 0; i < 4; ++i) {                       // R1: output X takes the smaller delay
         const uint4 d = s.d[i];
-        dtab[(i * 6 + 0) * dstride] = (T)d.z;
-        dtab[(i * 6 + 1) * dstride] = (T)d.w;
-        dtab[(i * 6 + 2) * dstride] = (T)min(d.z, d.w);
-        dtab[(i * 6 + 3) * dstride] = (T)d.x;
-        dtab[(i * 6 + 4) * dstride] = (T)d.y;
-        dtab[(i * 6 + 5) * dstride] = (T)min(d.x, d.y);
+        // (GLS_DELAY_INF -> 0xFFFF, above every finite delay of a gate on this path; the min
+        // for X then takes the related one)
+        const uint32_t z = min(d.z, 0xFFFFu), w = min(d.w, 0xFFFFu), x = min(d.x, 0xFFFFu), y = min(d.y, 0xFFFFu);
+        dtab[(i * 6 + 0) * dstride] = (T)z;
+        dtab[(i * 6 + 1) * dstride] = (T)w;
+        dtab[(i * 6 + 2) * dstride] = (T)min(z, w);
+        dtab[(i * 6 + 3) * dstride] = (T)x;
+        dtab[(i * 6 + 4) * dstride] = (T)y;
+        dtab[(i * 6 + 5) * dstride] = (T)min(x, y);
     }
 }
 
@@ -242,14 +254,15 @@ __device__ __noinline__ void fallback_count(const SimParams& p, Batch& B, int u,
     ChunkSetup s;
     unit_setup(p, B, u, s);
     ChunkOut r{0, 0, 0, 2, false};
-    B.u_deep[u] = 0xffffffffu;
+    WarpAux& X = warp_aux(p);
+    X.u_deep[u] = 0xffffffffu;
     run_chunk<false, false>(p, s, lut, nullptr, nullptr, 0, r);
     if (r.overflow) {
         const unsigned long long dcap = window_bound(p, s);
         const unsigned long long at = deep_alloc(p, dcap);
         r = ChunkOut{0, 0, 0, 2, false};
         if (at != ~0ull) {
-            B.u_deep[u] = (uint32_t)(at - (unsigned long long)warp_global_id() * p.deep_per_warp);
+            X.u_deep[u] = (uint32_t)(at - (unsigned long long)warp_global_id() * p.deep_per_warp);
             run_chunk<false, true>(p, s, lut, nullptr, p.deep + at, dcap, r);
         }
     }
@@ -263,12 +276,13 @@ __device__ __noinline__ void fallback_write(const SimParams& p, const Batch& B, 
     ChunkSetup s;
     unit_setup(p, B, u, s);
     ChunkOut r{0, 0, 0, 2, false};
-    if (B.u_deep[u] == 0xffffffffu) {
+    const uint32_t dofs = warp_aux(p).u_deep[u];
+    if (dofs == 0xffffffffu) {
         run_chunk<true, false>(p, s, lut, dst, nullptr, 0, r);
     } else {
         const unsigned long long dcap = window_bound(p, s);
         run_chunk<true, true>(p, s, lut, dst,
-                              p.deep + (unsigned long long)warp_global_id() * p.deep_per_warp + B.u_deep[u], dcap, r);
+                              p.deep + (unsigned long long)warp_global_id() * p.deep_per_warp + dofs, dcap, r);
     }
     if (r.cnt != B.u_cnt[u] || r.overflow) atomicOr(&p.ctl->error, kErrBug);
 }
@@ -388,8 +402,8 @@ __device__ __forceinline__ void unit_end(const SimParams& p, Batch& B, int u, ui
         // the fallback counts the whole unit again: take back what this partial run counted
         const int lane = threadIdx.x & 31;
         B.u_st[u] = 1;
-        B.lev[lane] -= B.lev[lane] + (l_cnt & 0xffffu) - B.u_sev[u];
-        B.levt[lane] -= B.levt[lane] + (l_cnt >> 16) - B.u_sevt[u];
+        B.lev[lane] -= B.lev[lane] + (l_cnt & 0xffffu) - warp_aux(p).u_sev[u];
+        B.levt[lane] -= B.levt[lane] + (l_cnt >> 16) - warp_aux(p).u_sevt[u];
         return;
     }
     const uint64_t* scr = p.wscr + sbase;
@@ -486,8 +500,8 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 t0q = ui.t0q;
                 lim = ui.lim;
                 asm volatile("" ::: "memory");                           // (keeps the copies in registers: ui is dead)
-                B.u_sev[u] = B.lev[lane];                                // counts so far (a fallback takes them back)
-                B.u_sevt[u] = B.levt[lane];
+                warp_aux(p).u_sev[u] = B.lev[lane];                      // counts so far (a fallback takes them back)
+                warp_aux(p).u_sevt[u] = B.levt[lane];
                 n = used;
                 nfl = used | (2u << 16);                                 // nothing final yet; value before: X
                 top = 0;
@@ -569,13 +583,14 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                     } while (cm);
                     const uint32_t rq = ((tq >> 2) + del) << 2;         // appearance time, entry form
                     // addSignalChange with Eq. 1: deny every pending schedule at >= rq
+                    // (del = 0xFFFF: every changed pin is unrelated, nothing scheduled, R9)
                     const uint32_t fl = nfl & 0xffffu;
-                    while (n > fl && top >= rq) {
+                    while (del != kDelayInf16 && n > fl && top >= rq) {
                         --n;
                         top = n > fl ? to_rel(ldg64(scr + n - 1), b4) : 0u;
                     }
                     const uint32_t tv = n > fl ? (top & 3u) : (nfl >> 16);
-                    if (tv != E) {                                       // push unless it repeats the tail
+                    if (tv != E && del != kDelayInf16) {                 // push unless it repeats the tail
                         if (n < (uint32_t)LCAP) {
                             top = rq | E;
                             stg64(scr + n, (uint64_t)top + b4);
@@ -738,6 +753,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             }
             const unsigned long long nch = __ldcg(&p.net_nck[p.P + g]);
             const unsigned long long e = __ldcg(&p.gate_nin[g]) / (nch ? nch : 1ull);
+            B.c_inf[nc] = (p.gate[g].flags & kGateInf) != 0;
             B.id[nc] = id;
             est[nc] = e;
             total += e;
@@ -752,14 +768,14 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         const unsigned long long w = max((unsigned long long)W_MIN, (total + 31) / 32);
         for (int j = 0; j < nc; ++j) {
             const unsigned long long e = est[j];
-            int ns = e >= w ? (int)min(32ull, max(1ull, (e + w / 2) / w)) : 1;
+            int ns = e >= w && !B.c_inf[j] ? (int)min(32ull, max(1ull, (e + w / 2) / w)) : 1;
             ns = min(ns, MAXU_STATIC - nu - (nc - 1 - j));           // room for the later chunks
             B.c_first[j] = (uint8_t)nu;
             B.c_nsl[j] = (uint8_t)ns;
             for (int q = 0; q < ns; ++q, ++nu) {
                 B.u_chunk[nu] = (uint8_t)j;
                 B.u_slice[nu] = (uint8_t)q;
-                B.u_est[nu] = (uint32_t)min(e / ns, 0xffffffffull);
+                B.u_est[nu] = B.c_inf[j] ? 0u : (uint32_t)min(e / ns, 0xffffffffull);   // (0: never split)
                 B.u_next[nu] = q + 1 < ns ? (uint8_t)(nu + 1) : kEnd;
                 B.u_st[nu] = 0;
                 B.u_lane[nu] = 0;

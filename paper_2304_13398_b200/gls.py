@@ -25,7 +25,9 @@ EXPORTS = ["gls_create", "gls_destroy", "gls_last_error", "gls_version", "gls_se
            "gls_simulate", "gls_simulate_window", "gls_get_waveforms", "gls_get_net_hashes", "gls_get_net_hashes_device",
            "gls_get_net_hashes_window", "gls_get_net_hash_terms_device",
            "gls_get_net_counts", "gls_get_stats", "gls_get_halo", "gls_get_levels", "gls_lut_lookup",
-           "gls_get_waveforms_range_device", "gls_scatter_segments"]
+           "gls_get_waveforms_range_device", "gls_scatter_segments", "gls_load_cells"]
+
+GLS_DELAY_INF = 0xFFFFFFFF
 
 
 class GlsError(RuntimeError):
@@ -39,6 +41,12 @@ class gls_config(ctypes.Structure):
                 ("chunk_events", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
                 ("ring_limit", ctypes.c_int32), ("engine", ctypes.c_int32), ("scheduler", ctypes.c_int32),
                 ("deep_per_warp", ctypes.c_int64), ("readback_mib", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class gls_cell_template(ctypes.Structure):
+    _fields_ = [("num_inputs", ctypes.c_int32), ("num_outputs", ctypes.c_int32), ("num_gates", ctypes.c_int32),
+                ("gate_type", ctypes.c_void_p), ("gate_fanin_offsets", ctypes.c_void_p),
+                ("gate_fanin", ctypes.c_void_p), ("output_node", ctypes.c_void_p)]
 
 
 class gls_stats(ctypes.Structure):
@@ -95,6 +103,7 @@ def load_library():
         "gls_lut_lookup": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, vp]),
         "gls_get_waveforms_range_device": (ctypes.c_int, [vp, i64, i64, i64, i64, vp, vp, i64, p(i64)]),
         "gls_scatter_segments": (ctypes.c_int, [vp, i64, vp, vp, vp, vp]),
+        "gls_load_cells": (ctypes.c_int, [vp, i32, i32, vp, i32, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -181,6 +190,34 @@ class Context:
         return self._check(self._lib.gls_load_netlist(self._h, int(num_inputs), int(gt.shape[0]),
                                                       gt.ctypes.data, fo.ctypes.data, fn.ctypes.data,
                                                       pd.ctypes.data))
+
+    def gls_load_cells(self, num_inputs, templates, cell_template, cell_fanin, cell_delay):
+        """templates: list of dict(n_in, n_out, gates=[(type, [node, ...]), ...], outputs=[node, ...])
+        (node ids: 0..n_in-1 cell inputs, n_in + j gate j); cell_delay: per cell the
+        [n_in][n_out][2 edge][2 value] block, concatenated (GLS_DELAY_INF = no relation)."""
+        keep = []
+        arr = (gls_cell_template * max(1, len(templates)))()
+        for i, t in enumerate(templates):
+            ty = _arr([g[0] for g in t["gates"]] or [0], np.uint8)
+            fo = np.zeros(len(t["gates"]) + 1, np.int32)
+            fo[1:] = np.cumsum([len(g[1]) for g in t["gates"]]) if t["gates"] else []
+            fi = _arr([x for g in t["gates"] for x in g[1]] or [0], np.int32)
+            on = _arr(t["outputs"], np.int32)
+            keep += [ty, fo, fi, on]
+            arr[i] = gls_cell_template(int(t["n_in"]), int(t["n_out"]), len(t["gates"]), ty.ctypes.data,
+                                       fo.ctypes.data, fi.ctypes.data, on.ctypes.data)
+        ct = _arr(cell_template, np.int32)
+        cf = _arr(cell_fanin, np.int32)
+        cd = _arr(cell_delay, np.uint32).reshape(-1)
+        if (ct.size and (ct.min() < 0 or ct.max() >= len(templates))) or \
+                cf.size != sum(templates[t]["n_in"] for t in ct) or \
+                cd.size != sum(4 * templates[t]["n_in"] * templates[t]["n_out"] for t in ct):
+            raise GlsError(GLS_EINVAL, "cell_template / cell_fanin / cell_delay do not match the templates")
+        rc = self._lib.gls_load_cells(self._h, int(num_inputs), len(templates), ctypes.addressof(arr), int(ct.shape[0]),
+                                      ct.ctypes.data, cf.ctypes.data, cd.ctypes.data)
+        self.num_inputs = int(num_inputs)
+        self.num_gates = int(sum(templates[t]["n_out"] for t in ct))
+        return self._check(rc)
 
     def load(self, nl):
         return self.gls_load_netlist(nl.num_inputs, nl.gate_type, nl.fanin_offsets, nl.fanin_net, nl.pin_delay)

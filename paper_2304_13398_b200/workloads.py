@@ -536,3 +536,49 @@ def wcv(lengths) -> float:
     (population sigma)."""
     x = np.asarray(lengths, np.float64)
     return float(x.std() / x.mean()) if x.size and x.mean() > 0 else 0.0
+
+
+# --------------------------------------------------------------------------
+# cell netlists (NEXT-2: multi-output cells / UDPs, 5-D delays with GLS_DELAY_INF)
+# --------------------------------------------------------------------------
+DELAY_INF = 0xFFFFFFFF
+
+# the full adder as one 3-input, 2-output cell template: sum = (a ^ b) ^ cin,
+# cout = (a & b) | ((a ^ b) & cin)
+FULL_ADDER = dict(n_in=3, n_out=2, gates=[(XOR, [0, 1]), (XOR, [3, 2]), (AND, [0, 1]), (AND, [3, 2]), (OR, [5, 6])],
+                  outputs=[4, 7])
+
+
+def random_template(rng, n_in, n_out, n_gates):
+    gates = []
+    for j in range(n_gates):
+        ty = int(rng.choice([BUF, NOT, AND, NAND, OR, NOR, XOR, XNOR, MUX2]))
+        k = 1 if ty in (BUF, NOT) else 3 if ty == MUX2 else int(rng.integers(2, 5))
+        nodes = [int(x) for x in rng.integers(0, n_in + j, size=k)]
+        gates.append((ty, nodes))
+    outs = [int(x) for x in rng.integers(max(0, n_in + n_gates - 3), n_in + n_gates, size=n_out)]
+    return dict(n_in=n_in, n_out=n_out, gates=gates, outputs=outs)
+
+
+def random_cells(seed, num_inputs, num_cells, max_delay=10, p_inf=0.15):
+    """A random cell library (a full adder, 3-input and 4-input UDPs with 1-3 outputs) and
+    a random DAG of cells over it; delays U[0, max_delay] per (in, out, edge, value),
+    GLS_DELAY_INF with probability p_inf.  Returns (templates, cell_tpl, cell_fanin,
+    cell_delay) — the arguments of gls_load_cells / oracle.simulate_cells."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    templates = [FULL_ADDER,
+                 random_template(rng, 2, 2, 3), random_template(rng, 3, 1, 4),
+                 random_template(rng, 3, 3, 5), random_template(rng, 4, 1, 4),
+                 dict(n_in=1, n_out=2, gates=[(NOT, [0])], outputs=[1, 0])]     # NOT + pass-through
+    cell_tpl, fanin, delay = [], [], []
+    nets = num_inputs
+    for _ in range(num_cells):
+        t = int(rng.integers(0, len(templates)))
+        tp = templates[t]
+        cell_tpl.append(t)
+        fanin += [int(x) for x in rng.integers(0, nets, size=tp["n_in"])]
+        d = rng.integers(0, max_delay + 1, size=tp["n_in"] * tp["n_out"] * 4).astype(np.uint64)
+        d[rng.random(d.size) < p_inf] = DELAY_INF
+        delay += [int(x) for x in d]
+        nets += tp["n_out"]
+    return templates, np.array(cell_tpl, np.int32), np.array(fanin, np.int32), np.array(delay, np.uint32)
