@@ -313,6 +313,7 @@ def run_gls(a):
         d_off, d_tr = W.window_stimuli(sp, *plan["gen_cycles"], dev)
         stims.append((d_off, d_tr, int(d_tr.numel())))
     torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()            # the generator's temporaries: leave the HBM to the library's arena
     d_off, d_tr, n_in = stims[0]
     lens = (d_off[1:] - d_off[:-1]).double()
     wcv = float(lens.std(unbiased=False) / lens.mean()) if n_in else 0.0

@@ -69,9 +69,15 @@ constexpr int MAXSPLIT = GLS_MAXSPLIT;           // splits per re-balancing poin
 #ifndef GLS_ADAPT
 #define GLS_ADAPT 1                              // batch fill adapts to the queue depth (dataflow scheduler)
 #endif
+#ifndef GLS_ADAPT_FILL
+#define GLS_ADAPT_FILL 1                         // expected entries a shallow-queue batch is filled to
+#endif
+#ifndef GLS_MAXU
+#define GLS_MAXU 64
+#endif
 constexpr int MAXC = 16;                         // chunks per batch
-constexpr int MAXU = 64;                         // units per batch (static + split)
-constexpr int MAXU_STATIC = 40;                  // static units per batch (the rest is room for splits)
+constexpr int MAXU = GLS_MAXU;                   // units per batch (static + split)
+constexpr int MAXU_STATIC = MAXU * 5 / 8;        // static units per batch (the rest is room for splits)
 constexpr uint8_t kEnd = 0xff;
 
 __device__ __forceinline__ uint64_t lds64(uint32_t a) {
@@ -697,7 +703,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         unsigned long long fill = 32ull * W_LANE;
         if (DATAFLOW && GLS_ADAPT) {
             const unsigned long long pub = ld_relaxed_u64(&p.ctl->chunk_top), head = ld_relaxed_u64(&p.ctl->work_head);
-            if (pub < head + (unsigned long long)gridDim.x * (blockDim.x >> 5)) fill = 1;
+            if (pub < head + (unsigned long long)gridDim.x * (blockDim.x >> 5)) fill = GLS_ADAPT_FILL;
         }
         while (nc < MAXC && total < fill) {
             unsigned long long id;

@@ -106,6 +106,8 @@ def load_library():
         "gls_load_cells": (ctypes.c_int, [vp, i32, i32, vp, i32, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
+        if os.environ.get("GLS_AB_OLD") and not hasattr(lib, name):
+            continue                    # A/B against an older build of the library (experiments only)
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

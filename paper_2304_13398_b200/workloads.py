@@ -239,6 +239,26 @@ def _epoch_of_cycle(k, L, phase):
     return torch.div(k + phase, L, rounding_mode="floor")
 
 
+def _cold_batch(spec, dev, pis, n_ep, e_lo, L, phase, off, cycle_lo, cycle_hi, tot, chunks, counts, p0):
+    """Epoch-toggling PIs of one batch: a transition at the first cycle of an epoch whose
+    level differs from the previous epoch's."""
+    rep = torch.repeat_interleave(torch.arange(pis.numel(), device=dev), n_ep)
+    start = torch.cumsum(n_ep, 0) - n_ep
+    e = e_lo[rep] + (torch.arange(tot, device=dev, dtype=torch.int64) - start[rep])
+    pi = pis[rep]
+    Lr, phr, offr = L[rep], phase[rep], off[rep]
+    k = torch.clamp(e * Lr - phr, min=0)           # first cycle of the epoch
+    ok = (k >= cycle_lo) & (k < cycle_hi) & (k < spec.ncycles)
+    cur = _level(spec, pi, e)
+    prv = torch.where(e == 0, torch.full_like(e, 2), _level(spec, pi, torch.clamp(e - 1, min=0)))
+    m = ok & (cur != prv)
+    pi, k, cur, offr = pi[m], k[m], cur[m], offr[m]
+    jit = _hash3(spec.seed, pi, k, _TAG_JIT) % 6
+    t = k * PERIOD + offr + jit
+    chunks.append((pi.to(torch.int32), (t << 2) | cur))
+    counts[p0:p0 + pis.numel()] += torch.bincount(pi - p0, minlength=pis.numel())
+
+
 def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
                      cycle_lo: int = 0, cycle_hi: int | None = None):
     """All transitions of every PI whose cycle lies in [cycle_lo, cycle_hi).
@@ -259,7 +279,9 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
     allp = torch.arange(P, device=dev, dtype=torch.int64)
     L_all, _, ph_all = _pi_params(spec, allp)
     span = max(1, cycle_hi - cycle_lo)
-    ep = torch.div(torch.full_like(allp, span), L_all, rounding_mode="floor") + 2
+    hot_all = torch.as_tensor(spec.hot if spec.hot is not None else np.zeros(P, np.int64), device=dev)
+    ep = torch.where(hot_all > 0, hot_all * span,                      # entries a batch generates per PI
+                     torch.div(torch.full_like(allp, span), L_all, rounding_mode="floor") + 2)
     cum = torch.cumsum(ep, 0).cpu().numpy()
     bounds, p0 = [], 0
     while p0 < P:
@@ -268,7 +290,6 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
         p1 = min(P, max(p1, p0 + 1), p0 + pi_batch)
         bounds.append((p0, p1))
         p0 = p1
-    hot_all = torch.as_tensor(spec.hot if spec.hot is not None else np.zeros(P, np.int64), device=dev)
     for p0, p1 in bounds:
         pis = torch.arange(p0, p1, device=dev, dtype=torch.int64)
         L, off, phase = _pi_params(spec, pis)
@@ -277,44 +298,29 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
         n_ep = torch.where(torch.full_like(pis, cycle_hi) > cycle_lo, e_hi - e_lo + 1, torch.zeros_like(pis))
         n_ep = torch.where(hot_all[p0:p1] > 0, torch.zeros_like(n_ep), n_ep)     # hot PIs: below
         tot = int(n_ep.sum().item())
-        if tot == 0:
-            continue
-        rep = torch.repeat_interleave(torch.arange(pis.numel(), device=dev), n_ep)
-        start = torch.cumsum(n_ep, 0) - n_ep
-        e = e_lo[rep] + (torch.arange(tot, device=dev, dtype=torch.int64) - start[rep])
-        pi = pis[rep]
-        Lr, phr, offr = L[rep], phase[rep], off[rep]
-        k = torch.clamp(e * Lr - phr, min=0)           # first cycle of the epoch
-        ok = (k >= cycle_lo) & (k < cycle_hi) & (k < spec.ncycles)
-        cur = _level(spec, pi, e)
-        prv = torch.where(e == 0, torch.full_like(e, 2), _level(spec, pi, torch.clamp(e - 1, min=0)))
-        m = ok & (cur != prv)
-        pi, k, cur, offr = pi[m], k[m], cur[m], offr[m]
-        jit = _hash3(spec.seed, pi, k, _TAG_JIT) % 6
-        t = k * PERIOD + offr + jit
-        chunks.append((pi, (t << 2) | cur))
-        counts[p0:p0 + pis.numel()] += torch.bincount(pi - p0, minlength=pis.numel())
-    # hot (clock-like) PIs: h transitions per cycle at offset_i + j * PERIOD / h, the value
-    # alternating 0/1 from a per-PI start bit (never X: every transition changes the value)
-    hp = torch.nonzero(hot_all > 0).flatten()
-    if hp.numel() and cycle_hi > cycle_lo:
-        h = hot_all[hp]
-        k_hi = min(cycle_hi, spec.ncycles)
-        per = (k_hi - cycle_lo) * h
-        tot = int(per.sum().item())
-        if tot:
-            rep = torch.repeat_interleave(torch.arange(hp.numel(), device=dev), per)
-            start = torch.cumsum(per, 0) - per
-            n = torch.arange(tot, device=dev, dtype=torch.int64) - start[rep] + cycle_lo * h[rep]   # global index
-            hr = h[rep]
-            k = torch.div(n, hr, rounding_mode="floor")
-            j = n - k * hr
-            pi = hp[rep]
-            _, off, _ = _pi_params(spec, pi)
-            sb = _hash3(spec.seed, pi, torch.zeros_like(pi), _TAG_LVL) & 1
-            t = k * PERIOD + off + j * torch.div(torch.full_like(hr, PERIOD), hr, rounding_mode="floor")
-            chunks.append((pi, (t << 2) | ((sb + n) & 1)))
-            counts.index_add_(0, hp, per)
+        if tot > 0:
+            _cold_batch(spec, dev, pis, n_ep, e_lo, L, phase, off, cycle_lo, cycle_hi, tot, chunks, counts, p0)
+        # hot (clock-like) PIs: h transitions per cycle at offset_i + j * PERIOD / h, the value
+        # alternating 0/1 from a per-PI start bit (never X: every transition changes the value)
+        hp = torch.nonzero(hot_all[p0:p1] > 0).flatten() + p0
+        if hp.numel() and cycle_hi > cycle_lo:
+            h = hot_all[hp]
+            k_hi = min(cycle_hi, spec.ncycles)
+            per = (k_hi - cycle_lo) * h
+            tot = int(per.sum().item())
+            if tot:
+                rep = torch.repeat_interleave(torch.arange(hp.numel(), device=dev), per)
+                start = torch.cumsum(per, 0) - per
+                n = torch.arange(tot, device=dev, dtype=torch.int64) - start[rep] + cycle_lo * h[rep]   # global index
+                hr = h[rep]
+                k = torch.div(n, hr, rounding_mode="floor")
+                j = n - k * hr
+                pi = hp[rep]
+                _, off, _ = _pi_params(spec, pi)
+                sb = _hash3(spec.seed, pi, torch.zeros_like(pi), _TAG_LVL) & 1
+                t = k * PERIOD + off + j * torch.div(torch.full_like(hr, PERIOD), hr, rounding_mode="floor")
+                chunks.append((pi.to(torch.int32), (t << 2) | ((sb + n) & 1)))
+                counts.index_add_(0, hp, per)
     offs = torch.zeros(P + 1, dtype=torch.int64, device=dev)
     offs[1:] = torch.cumsum(counts, 0)
     trans = torch.empty(int(offs[-1].item()), dtype=torch.int64, device=dev)
@@ -325,7 +331,8 @@ def generate_stimuli(spec: StimSpec, device="cpu", pi_batch=1 << 16,
         first = torch.ones_like(pi, dtype=torch.bool)
         first[1:] = pi[1:] != pi[:-1]
         gstart = torch.cummax(torch.where(first, torch.arange(pi.numel(), device=dev), torch.zeros_like(pi)), 0)[0]
-        trans[offs[pi] + (torch.arange(pi.numel(), device=dev) - gstart)] = e
+        trans[offs[pi.long()] + (torch.arange(pi.numel(), device=dev) - gstart)] = e
+    del chunks
     return offs, trans
 
 

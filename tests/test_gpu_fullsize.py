@@ -83,6 +83,7 @@ def test_full_size_windows_cover_ten_percent(cfg):
     spec = W.config_stimspec(cfg, 1)
     H = ctx.gls_get_halo()
     d_off, d_tr = W.window_stimuli(spec, 0, spec.ncycles, DEV)
+    torch.cuda.empty_cache()
     ctx.gls_set_input_waveforms_device(nl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), int(d_tr.numel()))
     ctx.gls_simulate(spec.duration)
     st = ctx.gls_get_stats()

@@ -83,7 +83,7 @@ def test_host_readback_in_small_batches(ctx):
     ctx.load(nl)
     ctx.gls_set_input_waveforms(nl.num_inputs, st.offsets, st.trans)
     ctx.gls_simulate(dur)
-    assert ref.trans.size > 3 * (1 << 17)                 # > 3 batches
+    assert ref.trans.size > (1 << 17)                     # > 1 batch of 1 MiB
     w = ctx.gls_get_waveforms()
     assert np.array_equal(w.offsets, ref.offsets) and np.array_equal(w.trans, ref.trans)
 
