@@ -98,7 +98,7 @@ typedef struct gls_config {
     int32_t readback_mib;    /* gls_get_waveforms: device staging buffer of the
                                 canonical CSR (MiB; batches of nets go through it,
                                 one D2H each); 0 = 1024                            */
-    int32_t reserved;
+    int32_t trace;           /* 1: record per-gate times for gls_get_trace (diagnostics) */
 } gls_config;
 
 typedef struct gls_stats {
@@ -310,6 +310,12 @@ int gls_get_stats(gls_ctx *ctx, gls_stats *out);
 /* 1 + maximum path delay (Σ of max pin delays along the worst path): the halo
  * that makes a time window exact (reading R17).  Needs a netlist. */
 int gls_get_halo(gls_ctx *ctx, int64_t *halo_ps);
+/* Scheduling trace of the last gls_simulate run with gls_config.trace = 1 (diagnostics,
+ * SURVEY §5 tracing): host uint64 [4 * num_gates], per gate in the caller's order:
+ * %globaltimer ns when the gate was planned (its chunks published, Alg. 1's unlock),
+ * when its last chunk completed, the sum and the maximum of its chunks' durations
+ * (claim to completion, ns).  GLS_ESTATE without a traced result. */
+int gls_get_trace(gls_ctx *ctx, uint64_t *trace);
 /* Number of topological levels of the loaded netlist (0 without gates). */
 int gls_get_levels(gls_ctx *ctx, int32_t *levels);
 

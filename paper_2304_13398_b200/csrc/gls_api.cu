@@ -167,6 +167,8 @@ struct gls_ctx {
     DevBuf<uint8_t> d_ck_vb;
     DevBuf<uint64_t> d_deep;
     DevBuf<uint64_t> d_wscr;
+    DevBuf<unsigned long long> d_trace;     // gls_config.trace
+    bool traced = false;
     DevBuf<unsigned char> d_waux;
     DevBuf<uint64_t> d_hash;                // result checksums (kept: no malloc/free per readback)
     DevBuf<Ctl> d_ctl;
@@ -242,6 +244,7 @@ SimParams params(gls_ctx* ctx) {
     p.deep = ctx->d_deep.p;
     p.wscr = ctx->d_wscr.p;
     p.waux = ctx->d_waux.p;
+    p.trace = ctx->cfg.trace ? ctx->d_trace.p : nullptr;
     p.deep_wtop = ctx->d_deep_wtop.p;
     p.fo_off = ctx->d_fo_off.p;
     p.fo_gate = ctx->d_fo_gate.p;
@@ -416,7 +419,8 @@ int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
     if (!ctx || !cfg) return GLS_EINVAL;
     if (cfg->arena_bytes < 0 || cfg->chunk_capacity < 0 || cfg->chunk_events < 0 || cfg->blocks_per_sm < 0 ||
         cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 1 ||
-        cfg->scheduler < 0 || cfg->scheduler > 1 || cfg->deep_per_warp < 0 || cfg->readback_mib < 0)
+        cfg->scheduler < 0 || cfg->scheduler > 1 || cfg->deep_per_warp < 0 || cfg->readback_mib < 0 ||
+        cfg->trace < 0 || cfg->trace > 1)
         return fail(ctx, GLS_EINVAL, "invalid gls_config field");
     ctx->cfg = *cfg;
     ctx->deep_per_warp = 0;                  // re-derived from cfg at the next simulate
@@ -899,6 +903,13 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
         init.work_head = (unsigned long long)ctx->P;
         init.arena_top = (unsigned long long)((ctx->prefix_total + 15) & ~15ll);   // 128-byte segments
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        if (ctx->cfg.trace) {
+            CK(ctx->d_trace.ensure((size_t)4 * std::max<int32_t>(ctx->G, 1)));
+            CK(cudaMemsetAsync(ctx->d_trace.p, 0, sizeof(unsigned long long) * 4 * std::max<int32_t>(ctx->G, 1),
+                               ctx->stream));
+            p.trace = ctx->d_trace.p;
+        }
+        ctx->traced = ctx->cfg.trace != 0;
         CK(cudaMemcpyAsync(ctx->d_ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemsetAsync(ctx->d_work.p, 0, sizeof(unsigned long long) * (ctx->L + 1), ctx->stream));
         if (ctx->G > 0) {
@@ -998,6 +1009,16 @@ int gls_get_stats(gls_ctx* ctx, gls_stats* out) {
         ctx->stats.fanin_reads = (int64_t)reads;
     }
     *out = ctx->stats;
+    return GLS_OK;
+}
+
+int gls_get_trace(gls_ctx* ctx, uint64_t* trace) {
+    if (!ctx || !trace) return GLS_EINVAL;
+    if (!ctx->has_result || !ctx->traced) return fail(ctx, GLS_ESTATE, "no traced simulation result (gls_config.trace)");
+    std::vector<unsigned long long> t((size_t)4 * ctx->G);
+    if (ctx->G) CK(cudaMemcpy(t.data(), ctx->d_trace.p, sizeof(unsigned long long) * 4 * ctx->G, cudaMemcpyDeviceToHost));
+    for (int32_t g = 0; g < ctx->G; ++g)
+        for (int q = 0; q < 4; ++q) trace[4ll * g + q] = t[4ll * ctx->inv[g] + q];
     return GLS_OK;
 }
 

@@ -45,15 +45,23 @@ constexpr uint8_t kGateInf = 1;
 enum : unsigned { kErrArena = 1u, kErrChunks = 2u, kErrDeep = 4u, kErrInput = 8u, kErrBug = 16u, kErrWatchdog = 32u };
 
 // device control block, initialised by the host before each run
+// (the counters every warp hits — atomics on the queue and the store, the polled completion
+// count — each own a 128-byte line: one hot line would serialise all of them in one L2 slice)
 struct Ctl {
     unsigned long long chunk_top;   // next free chunk id (starts at P: one chunk per given net)
+    unsigned long long pad0[15];
     unsigned long long arena_top;   // next free arena entry (starts after the given waveforms)
+    unsigned long long pad1[15];
     unsigned long long work_head;   // dataflow queue: next chunk id to hand out (starts at P)
+    unsigned long long pad2[15];
     unsigned long long done_gates;  // dataflow: completed gates
+    unsigned int error;             // kErr* bits
+    unsigned int pad3a;
+    unsigned long long pad3[14];
     unsigned int bar_count;
     unsigned int bar_gen;
     unsigned int bar_abort;
-    unsigned int error;             // kErr* bits
+    unsigned int pad4;
     unsigned long long need_arena;  // entries needed when kErrArena was raised
     unsigned long long need_chunks;
     unsigned long long need_deep;
@@ -109,6 +117,7 @@ struct SimParams {
     int32_t engine;             // 0 = lanes on re-balanced units, 1 = per-lane chunks
     int32_t sched;              // 0 = dataflow (ready counters), 1 = level barriers
     uint32_t nblocks;
+    unsigned long long* trace;  // [4 G] or null: plan time, completion time, Σ / max chunk durations (ns)
 };
 
 // kernels / launchers (gls_kernels.cu)

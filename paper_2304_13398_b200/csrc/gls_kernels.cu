@@ -69,6 +69,11 @@ __device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
 // release fence without the L1 invalidation a full __threadfence() implies
 __device__ __forceinline__ void fence_release() { asm volatile("fence.release.gpu;" ::: "memory"); }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ unsigned warp_global_id() { return blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); }
 
 // Device-wide barrier for a co-resident (cooperative) grid.  The last block to
@@ -683,6 +688,7 @@ __device__ void plan_gate(const SimParams& p, uint32_t c) {
         return;
     }
     if (lane == 0) {
+        if (p.trace) p.trace[4ull * c] = gtimer();
         p.net_ck[p.P + c] = (uint32_t)base;
         p.net_nck[p.P + c] = (uint32_t)nch;
         p.gate_nin[c] = n_in;
@@ -717,7 +723,10 @@ __device__ void gate_complete(const SimParams& p, uint32_t gi, uint32_t base, ui
         if (j < nch) p.ck_cum[base + j] = cum + x - c;
         cum += __shfl_sync(0xffffffffu, x, 31);
     }
-    if (lane == 0) p.net_len[p.P + gi] = cum;
+    if (lane == 0) {
+        p.net_len[p.P + gi] = cum;
+        if (p.trace) p.trace[4ull * gi + 1] = gtimer();
+    }
     if (!DATAFLOW) return;
     fence_release();
     __syncwarp();

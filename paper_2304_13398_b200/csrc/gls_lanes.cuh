@@ -42,15 +42,19 @@ constexpr uint32_t kRebaseQ = 0x80000000u;       // entry form of t - B = 2^29
 constexpr uint32_t kFastDelay = 0xFFFFu;         // gates with dmax below this use the 32-bit sweep (u16 delays;
                                                  // 0xFFFF there = GLS_DELAY_INF)
 #ifndef GLS_LCAP
-#define GLS_LCAP 2048
+#define GLS_LCAP 4096
 #endif
 constexpr int LCAP = GLS_LCAP;                   // per-lane output scratch (stack) entries
+constexpr unsigned long long U_MAX = LCAP / 4;   // most expected entries of a static unit
 constexpr size_t kScratchPerWarp = 32u * LCAP;
 #ifndef GLS_WLANE
 #define GLS_WLANE 256
 #endif
 constexpr int W_LANE = GLS_WLANE;                // a batch is filled up to 32 x W_LANE expected entries
-constexpr int W_MIN = 32;                        // fewest expected entries per static unit
+#ifndef GLS_WMIN
+#define GLS_WMIN 32
+#endif
+constexpr int W_MIN = GLS_WMIN;                  // fewest expected entries per static unit
 #ifndef GLS_ROUND
 #define GLS_ROUND 32
 #endif
@@ -171,12 +175,15 @@ struct Batch {
     uint32_t c_total[MAXC];
     uint8_t c_first[MAXC], c_nsl[MAXC];    // first unit, static slices
     uint8_t c_inf[MAXC];                   // the chunk's gate has a GLS_DELAY_INF pin: one unit, never split
+    unsigned long long c_t[MAXC];          // claim time (gls_config.trace)
     long long u_T0[MAXU], u_T1[MAXU];      // unit time range
     uint32_t u_soff[MAXU], u_cnt[MAXU];    // outputs: lane-scratch offset, count
     uint32_t u_pre[MAXU];                  // offset of the unit's outputs inside its chunk
     uint32_t u_est[MAXU];                  // expected merged entries
     uint8_t u_chunk[MAXU], u_slice[MAXU], u_lane[MAXU], u_vb[MAXU], u_st[MAXU], u_next[MAXU];
     int qhead;                             // next static unit to hand out
+    int round;                             // re-balancing rounds of the batch so far
+    uint16_t u_r0[MAXU];                   // round in which the unit started
     int nun;                               // units (static + split)
     int8_t pend[32];                       // unit handed to a lane by a split (-1: none)
     uint32_t lev[32], levt[32];            // per-lane gate-evals / events of the batch
@@ -304,6 +311,65 @@ __device__ __forceinline__ void thresholds(uint64_t b4, long long T0, long long 
     lim = more ? kRebaseQ : (a2 <= 0 ? 0u : (uint32_t)(a2 << 2));
 }
 
+// Cursors of all k pins at tau0 (as locate(), gls_kernels.cu): the binary searches over
+// the chunk start times and then inside the segments advance in lockstep, so the k chains
+// of dependent global loads overlap — the set-up latency of a unit is about one search,
+// not k.
+__device__ __forceinline__ void locate_all(const SimParams& p, const uint32_t* src, uint32_t k, long long tau0,
+                                           Cursor* c, uint32_t* init) {
+    uint32_t cb[4], lo[4], hi[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        cb[i] = (uint32_t)i < k ? __ldcg(&p.net_ck[src[i]]) : 0u;
+        lo[i] = 0;
+        hi[i] = (uint32_t)i < k ? __ldcg(&p.net_nck[src[i]]) : 1u;
+        c[i].ck_end = cb[i] + hi[i];
+    }
+    for (;;) {                                      // largest j with ck_T[j] <= tau0 + 1 (default 0)
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (hi[i] - lo[i] > 1) {
+                any = true;
+                const uint32_t mid = (lo[i] + hi[i]) >> 1;
+                if (__ldcg(&p.ck_T[cb[i] + mid]) <= tau0 + 1) lo[i] = mid; else hi[i] = mid;
+            }
+        }
+        if (!any) break;
+    }
+    const uint64_t* seg[4];
+    uint32_t a[4], b[4], cnt[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t j = cb[i] + lo[i];
+        seg[i] = (uint32_t)i < k ? p.arena + __ldcg(&p.ck_off[j]) : p.arena;
+        cnt[i] = (uint32_t)i < k ? __ldcg(&p.ck_cnt[j]) : 0u;
+        a[i] = 0;
+        b[i] = cnt[i];
+        c[i].ck = j;
+    }
+    for (;;) {                                      // first index with t > tau0
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (a[i] < b[i]) {
+                any = true;
+                const uint32_t m = (a[i] + b[i]) >> 1;
+                if (etime(seg[i][m]) <= tau0) a[i] = m + 1; else b[i] = m;
+            }
+        }
+        if (!any) break;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if ((uint32_t)i >= k) continue;
+        init[i] = a[i] > 0 ? (uint32_t)(seg[i][a[i] - 1] & 3u) : (uint32_t)__ldcg(&p.ck_vb[c[i].ck]);
+        c[i].ptr = seg[i] + a[i];
+        c[i].end = seg[i] + cnt[i];
+        refill(p, c[i]);
+    }
+}
+
 // Start unit u on this lane (the set-up path, kept out of the sweep's registers):
 // its delay table, the cursors of its pins at tau0 = T0 - dmax - 1 (binary search over
 // chunk start times, then inside the segment; value in effect from ck_vb), the first
@@ -333,6 +399,9 @@ __device__ __noinline__ bool unit_begin(const SimParams& p, int u, UnitInit& o) 
     const uint64_t b4 = (uint64_t)s.tau0 << 2;
     o.b4 = b4;
     uint32_t xn = 0, xr0 = 0;
+    Cursor cur[4];
+    uint32_t ini[4];
+    locate_all(p, s.src, s.k, s.tau0, cur, ini);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int ci = i * kThreads + tid;
@@ -340,9 +409,8 @@ __device__ __noinline__ bool unit_begin(const SimParams& p, int u, UnitInit& o) 
         if ((uint32_t)i >= s.k) {
             sts32(cs.rem(ci), 0u);                                       // absent pin: exhausted
         } else {
-            Cursor cc;
-            uint32_t init;
-            locate(p, s.src[i], s.tau0, cc, init);
+            const Cursor& cc = cur[i];
+            const uint32_t init = ini[i];
             const uint32_t rem = (uint32_t)(cc.end - cc.ptr);
             sts64(cs.ptr(ci), (uint64_t)cc.ptr);
             sts32(cs.rem(ci), rem);
@@ -507,6 +575,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 lim = ui.lim;
                 asm volatile("" ::: "memory");                           // (keeps the copies in registers: ui is dead)
                 warp_aux(p).u_sev[u] = B.lev[lane];                      // counts so far (a fallback takes them back)
+                B.u_r0[u] = (uint16_t)B.round;
                 warp_aux(p).u_sevt[u] = B.levt[lane];
                 n = used;
                 nfl = used | (2u << 16);                                 // nothing final yet; value before: X
@@ -623,6 +692,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 B.acc[A_WARP_IT] += 32ull * itmax;
                 B.acc[A_LANE_IT] += itsum;
                 B.acc[A_BAL + 2] += 1ull;
+                B.round = min(B.round + 1, 65535);
             }
         }
         const bool qempty = *(volatile int*)&B.qhead >= nstatic;
@@ -634,13 +704,21 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         }
         // idle lanes take the upper half (in time) of the busiest lanes' remaining ranges
         float re = 0.f;
-        long long tn = 0, T1u = 0;
+        long long tn = 0, T1u = 0, ts = 0;
         if (u >= 0 && m < lim) {
             const long long T0u = B.u_T0[u];
             T1u = B.u_T1[u];
             tn = ((long long)b4 >> 2) + (long long)(m >> 2);             // next timestamp to process
-            if (tn >= T0u && T1u - tn >= 2)                              // expected entries, by the time left
-                re = (float)B.u_est[u] * (float)(T1u - tn) / (float)max(1ll, T1u - T0u);
+            if (tn >= T0u && T1u - tn >= 2 && B.u_est[u]) {
+                // entries left: the unit's estimate scaled by the time left, or the lane's own
+                // pace so far (ROUND iterations per round since the unit started) if larger —
+                // an estimate from the chunk average misses bursts inside the unit
+                const float left = (float)(T1u - tn);
+                const float est = (float)B.u_est[u] * left / (float)max(1ll, T1u - T0u);
+                const float done = ((float)(B.round - (int)B.u_r0[u]) + 0.5f) * (float)ROUND;
+                re = fmaxf(est, done * left / (float)max(1ll, tn - T0u));
+                ts = tn + (T1u - tn) / 2;                                 // > every timestamp applied so far
+            }
         }
         unsigned rcv = idle;
         int nun = B.nun;
@@ -651,7 +729,6 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
             const int rl = __ffs(rcv) - 1;
             rcv &= rcv - 1;
             if (lane == dl) {
-                const long long ts = tn + (T1u - tn) / 2;                // > every timestamp applied so far
                 B.u_T0[nun] = ts;
                 B.u_T1[nun] = T1u;
                 B.u_chunk[nun] = B.u_chunk[u];
@@ -698,6 +775,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         // ---- claim published chunks until the batch holds about 32 x W_LANE expected entries
         unsigned long long est[MAXC];
         unsigned long long total = 0;
+        int units_needed = 0;
         // shallow queue (fewer published chunks than warps): one chunk per batch, so its
         // units spread over all 32 lanes and the critical path through the netlist shortens
         unsigned long long fill = 32ull * W_LANE;
@@ -711,7 +789,16 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
                 id = carry;
                 carry = NONE;
             } else if (DATAFLOW) {
-                id = atomicAdd(&p.ctl->work_head, 1ull);
+                if (nc == 0) {
+                    id = atomicAdd(&p.ctl->work_head, 1ull);    // (an idle warp may wait for its id)
+                } else {
+                    // a busy warp never holds an unpublished id (its consumers would wait for
+                    // this whole batch): take the head only if published, by compare-and-swap
+                    const unsigned long long h = ld_relaxed_u64(&p.ctl->work_head);
+                    if (h >= p.ck_cap || ld_relaxed_u32(&p.ck_gate[h]) == 0xffffffffu) break;
+                    if (atomicCAS(&p.ctl->work_head, h, h + 1ull) != h) break;
+                    id = h;
+                }
             } else {
                 const unsigned long long w = atomicAdd(lvl_work, 1ull);
                 if (w >= lvl_n) break;
@@ -725,23 +812,28 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
                         carry = id;
                         break;
                     }
-                    unsigned ns = 32;
+                    // wait for the claimed id to be published: poll its own ck_gate word
+                    // (every waiting warp a different line); the shared completion count and
+                    // error word only every 16th poll
+                    unsigned ns = 64, polls = 0;
                     unsigned long long t_start = 0, seen = ~0ull;
                     for (;;) {
                         if (id < p.ck_cap) {
                             g = ld_relaxed_u32(&p.ck_gate[id]);   // (polls stay relaxed: an acquire
                             if (g != 0xffffffffu) break;            //  invalidates the SM's L1 each time)
                         }
-                        const unsigned long long done = ld_relaxed_u64(&p.ctl->done_gates);
-                        if (done >= (unsigned long long)p.G || ld_relaxed_u32(&p.ctl->error) != 0u) break;
-                        unsigned long long now;             // watchdog (10 s without progress)
-                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
-                        if (done != seen) {
-                            seen = done;
-                            t_start = now;
-                        } else if (now - t_start > 10000000000ull) {
-                            atomicOr(&p.ctl->error, kErrWatchdog);
-                            break;
+                        if ((++polls & 15u) == 0u || id >= p.ck_cap) {
+                            const unsigned long long done = ld_relaxed_u64(&p.ctl->done_gates);
+                            if (done >= (unsigned long long)p.G || ld_relaxed_u32(&p.ctl->error) != 0u) break;
+                            unsigned long long now;             // watchdog (10 s without progress)
+                            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                            if (done != seen) {
+                                seen = done;
+                                t_start = now;
+                            } else if (now - t_start > 10000000000ull) {
+                                atomicOr(&p.ctl->error, kErrWatchdog);
+                                break;
+                            }
                         }
                         __nanosleep(ns);
                         if (ns < GLS_MAXSLEEP) ns <<= 1;
@@ -759,8 +851,17 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             }
             const unsigned long long nch = __ldcg(&p.net_nck[p.P + g]);
             const unsigned long long e = __ldcg(&p.gate_nin[g]) / (nch ? nch : 1ull);
+            // static units of at most U_MAX expected entries (a unit's outputs must fit the lane
+            // scratch); a chunk that would not fit the batch's unit budget waits for the next batch
+            const int need = (int)min(32ull, max(1ull, (e + U_MAX - 1) / U_MAX));
+            if (nc > 0 && units_needed + need > MAXU_STATIC) {
+                carry = id;
+                break;
+            }
+            units_needed += need;
             B.c_inf[nc] = (p.gate[g].flags & kGateInf) != 0;
             B.id[nc] = id;
+            B.c_t[nc] = p.trace ? gtimer() : 0ull;
             est[nc] = e;
             total += e;
             ++nc;
@@ -775,7 +876,8 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         for (int j = 0; j < nc; ++j) {
             const unsigned long long e = est[j];
             int ns = e >= w && !B.c_inf[j] ? (int)min(32ull, max(1ull, (e + w / 2) / w)) : 1;
-            ns = min(ns, MAXU_STATIC - nu - (nc - 1 - j));           // room for the later chunks
+            if (!B.c_inf[j]) ns = max(ns, (int)min(32ull, (e + U_MAX - 1) / U_MAX));
+            ns = max(1, min(ns, MAXU_STATIC - nu - (nc - 1 - j)));   // room for the later chunks
             B.c_first[j] = (uint8_t)nu;
             B.c_nsl[j] = (uint8_t)ns;
             for (int q = 0; q < ns; ++q, ++nu) {
@@ -788,6 +890,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             }
         }
         B.qhead = 0;
+        B.round = 0;
         B.acc[A_BAL + 0] += (unsigned long long)nu;
         B.acc[A_BLANES] += (unsigned long long)min(nu, 32);
         p.deep_wtop[warp_global_id()] = 0;          // this warp's deep scratch, reused per batch
@@ -891,6 +994,11 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         R.vb = B.u_vb[B.c_first[j]];
         R.evals = 0;                                   // (counted per lane above)
         R.events = 0;
+        if (p.trace && lane == 0) {
+            const unsigned long long d = gtimer() - B.c_t[j];
+            atomicAdd(&p.trace[4ull * R.gi + 2], d);
+            atomicMax(&p.trace[4ull * R.gi + 3], d);
+        }
         chunk_done<DATAFLOW>(p, id, R, B.acc);
     }
     const long long c_end = clock64();

@@ -25,7 +25,7 @@ EXPORTS = ["gls_create", "gls_destroy", "gls_last_error", "gls_version", "gls_se
            "gls_simulate", "gls_simulate_window", "gls_get_waveforms", "gls_get_net_hashes", "gls_get_net_hashes_device",
            "gls_get_net_hashes_window", "gls_get_net_hash_terms_device",
            "gls_get_net_counts", "gls_get_stats", "gls_get_halo", "gls_get_levels", "gls_lut_lookup",
-           "gls_get_waveforms_range_device", "gls_scatter_segments", "gls_load_cells"]
+           "gls_get_waveforms_range_device", "gls_scatter_segments", "gls_load_cells", "gls_get_trace"]
 
 GLS_DELAY_INF = 0xFFFFFFFF
 
@@ -40,7 +40,7 @@ class gls_config(ctypes.Structure):
     _fields_ = [("arena_bytes", ctypes.c_int64), ("chunk_capacity", ctypes.c_int64),
                 ("chunk_events", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
                 ("ring_limit", ctypes.c_int32), ("engine", ctypes.c_int32), ("scheduler", ctypes.c_int32),
-                ("deep_per_warp", ctypes.c_int64), ("readback_mib", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("deep_per_warp", ctypes.c_int64), ("readback_mib", ctypes.c_int32), ("trace", ctypes.c_int32)]
 
 
 class gls_cell_template(ctypes.Structure):
@@ -104,6 +104,7 @@ def load_library():
         "gls_get_waveforms_range_device": (ctypes.c_int, [vp, i64, i64, i64, i64, vp, vp, i64, p(i64)]),
         "gls_scatter_segments": (ctypes.c_int, [vp, i64, vp, vp, vp, vp]),
         "gls_load_cells": (ctypes.c_int, [vp, i32, i32, vp, i32, vp, vp, vp]),
+        "gls_get_trace": (ctypes.c_int, [vp, vp]),
     }
     for name, (res, args) in sig.items():
         if os.environ.get("GLS_AB_OLD") and not hasattr(lib, name):
@@ -178,9 +179,9 @@ class Context:
 
     # ---- ABI calls ----------------------------------------------------------
     def gls_set_config(self, arena_bytes=0, chunk_capacity=0, chunk_events=0, blocks_per_sm=0, ring_limit=0,
-                       engine=0, scheduler=0, deep_per_warp=0, readback_mib=0):
+                       engine=0, scheduler=0, deep_per_warp=0, readback_mib=0, trace=0):
         c = gls_config(arena_bytes, chunk_capacity, chunk_events, blocks_per_sm, ring_limit, engine, scheduler,
-                       deep_per_warp, readback_mib)
+                       deep_per_warp, readback_mib, trace)
         return self._check(self._lib.gls_set_config(self._h, ctypes.byref(c)))
 
     def gls_load_netlist(self, num_inputs, gate_type, fanin_offsets, fanin_net, pin_delay):
@@ -291,6 +292,11 @@ class Context:
         s = gls_stats()
         self._check(self._lib.gls_get_stats(self._h, ctypes.byref(s)))
         return s.as_dict()
+
+    def gls_get_trace(self) -> np.ndarray:
+        t = np.zeros((self.num_gates, 4), np.uint64)
+        self._check(self._lib.gls_get_trace(self._h, t.ctypes.data))
+        return t
 
     def gls_get_halo(self) -> int:
         h = ctypes.c_int64()
