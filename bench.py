@@ -345,7 +345,7 @@ def run_gls(a):
         log(f"warmup {i}: kernel {s['kernel_ms']:.1f} ms, {s['gate_evals']} gate-evals, "
             f"{s['out_transitions']} outputs, {s['chunks']} chunks ({s['deep_chunks']} fallback), "
             f"lane util {s['lane_utilization']:.2f}, batches {s['batches']} x {s['batch_lanes']:.1f} lanes / "
-            f"{s['batch_est']:.0f} est, phases {[round(x / max(1.0, sum(s['phase_cycles'])), 3) for x in s['phase_cycles']]}, "
+            f"{s['batch_est']:.0f} est, phases {[round(x / max(1.0, sum(s['phase_cycles'][:5])), 3) for x in s['phase_cycles']]}, "
             f"arena {s['arena_used_bytes'] / 1e9:.1f} GB, balance {balance_str(s)} "
             f"(wall {time.perf_counter() - t:.2f}s)")
     if world > 1:

@@ -88,7 +88,10 @@ typedef struct gls_config {
     int32_t engine;          /* evaluation engine of a (gate, time-chunk) item:
                                 0 = a warp's lanes on time-slice units of a batch of
                                     items, re-balanced by splitting while they run (default),
-                                1 = one item per lane (reference engine for A/B)      */
+                                1 = one item per lane (reference engine for A/B),
+                                2 = the paper's design (A/B): CSRP pages with next-page
+                                    pointers and an atomic page iterator (§3.1), one
+                                    thread per cell statically dealt (Alg. 1)            */
     int32_t scheduler;       /* 0 = dataflow: a gate is scheduled when its last fan-in
                                 gate completes (Alg. 1 unlock rule) (default);
                                 1 = topological levels separated by device barriers.
@@ -99,6 +102,7 @@ typedef struct gls_config {
                                 canonical CSR (MiB; batches of nets go through it,
                                 one D2H each); 0 = 1024                            */
     int32_t trace;           /* 1: record per-gate times for gls_get_trace (diagnostics) */
+    int32_t csrp_pagelen;    /* engine 2: CSRP page length in entries (256); 0 = 256 */
 } gls_config;
 
 typedef struct gls_stats {
@@ -121,11 +125,15 @@ typedef struct gls_stats {
     double batch_est;        /* engine 0: mean expected merged entries per batch    */
     double phase_cycles[6];  /* engine 0, lane 0 clocks summed over warps: waiting +
                                 batch assembly, static unit boundaries, sweep (rounds),
-                                fallback + allocation + output copy, chunk completion, - */
+                                fallback + allocation + output copy, chunk completion,
+                                lane-average clocks in unit set-up (part of the sweep) */
     double balance[8];       /* engine 0 counters: [0] static units, [1] units split off
                                 while running, [2] re-balancing rounds, [3] fallback
                                 units (per-lane ring engine), [4]-[7] unused          */
     double kernel_ms;        /* CUDA-event time of the gate-evaluation kernel      */
+    int64_t csrp_pages;      /* engine 2: CSRP pages handed out                     */
+    int64_t csrp_waste;      /* engine 2: page slots not holding an entry (Eq. 4 bounds
+                                it by pagelen x waveforms)               */
     double simulate_ms;      /* CUDA-event time of the whole gls_simulate          */
 } gls_stats;
 

@@ -168,6 +168,9 @@ struct gls_ctx {
     DevBuf<uint64_t> d_deep;
     DevBuf<uint64_t> d_wscr;
     DevBuf<unsigned long long> d_trace;     // gls_config.trace
+    DevBuf<uint64_t> d_pages;               // engine 2: CSRP pages
+    DevBuf<unsigned long long> d_first_page, d_out_cnt, d_seg_off;
+    DevBuf<uint32_t> d_known;
     bool traced = false;
     DevBuf<unsigned char> d_waux;
     DevBuf<uint64_t> d_hash;                // result checksums (kept: no malloc/free per readback)
@@ -418,9 +421,9 @@ void gls_destroy(gls_ctx* ctx) {
 int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
     if (!ctx || !cfg) return GLS_EINVAL;
     if (cfg->arena_bytes < 0 || cfg->chunk_capacity < 0 || cfg->chunk_events < 0 || cfg->blocks_per_sm < 0 ||
-        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 1 ||
+        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 2 ||
         cfg->scheduler < 0 || cfg->scheduler > 1 || cfg->deep_per_warp < 0 || cfg->readback_mib < 0 ||
-        cfg->trace < 0 || cfg->trace > 1)
+        cfg->trace < 0 || cfg->trace > 1 || cfg->csrp_pagelen == 1 || cfg->csrp_pagelen < 0)
         return fail(ctx, GLS_EINVAL, "invalid gls_config field");
     ctx->cfg = *cfg;
     ctx->deep_per_warp = 0;                  // re-derived from cfg at the next simulate
@@ -877,10 +880,13 @@ int gls_simulate_window(gls_ctx* ctx, int64_t t_begin, int64_t t_end, int64_t du
     return simulate_run(ctx, sim);
 }
 
+static int simulate_csrp(gls_ctx* ctx, int64_t duration);
+
 static int simulate_run(gls_ctx* ctx, int64_t duration) {
     cudaSetDevice(ctx->device);
     ctx->has_result = false;
     ctx->duration = duration;
+    if (ctx->cfg.engine == 2) return simulate_csrp(ctx, duration);
     int rc = ensure_chunks(ctx, 0);
     if (rc) return rc;
     int per_sm = 0;
@@ -990,6 +996,90 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
         return GLS_OK;
     }
     return fail(ctx, GLS_ENOMEM, "simulation did not fit after resizing");
+}
+
+
+// Engine 2 (NEXT-3): the paper's CSRP store and Alg. 1 (gls_csrp.cuh) — given waveforms
+// copied into pages, one cooperative launch, then the pages of every gate output collected
+// into exact arena segments (one chunk per net) for the library's readers.
+static int simulate_csrp(gls_ctx* ctx, int64_t duration) {
+    const int32_t P = ctx->P, G = ctx->G;
+    const int64_t N = (int64_t)P + G;
+    const uint32_t L = ctx->cfg.csrp_pagelen > 0 ? (uint32_t)ctx->cfg.csrp_pagelen : 256u;
+    int rc = ensure_chunks(ctx, 0);
+    if (rc) return rc;
+    const int threads = csrp_coresident_threads(ctx->device);
+    if (threads < 1) return fail(ctx, GLS_ECUDA, "CSRP kernel cannot be resident");
+    if (ctx->d_wscr.n < csrp_scratch_entries(threads)) CK(ctx->d_wscr.alloc(csrp_scratch_entries(threads)));
+    // pages: the arena's room for outputs plus the given waveforms, and one page per waveform
+    // of slack (Eq. 4's waste bound)
+    const int64_t room = (int64_t)ctx->d_arena.n - ctx->prefix_total;
+    int64_t want = (ctx->prefix_total + std::max<int64_t>(room, 0)) / (int64_t)(L - 1) + 2 * N + 16;
+    const int64_t fit = (int64_t)(0.45 * (double)free_bytes(ctx)) / (8 * (int64_t)L);
+    want = std::max<int64_t>(16, std::min(want, fit));
+    if ((int64_t)ctx->d_pages.n < want * (int64_t)L) CK(ctx->d_pages.alloc((size_t)want * L));
+    const unsigned long long page_cap = ctx->d_pages.n / L;
+    CK(ctx->d_first_page.ensure((size_t)N + 1));
+    CK(ctx->d_out_cnt.ensure((size_t)N + 1));
+    CK(ctx->d_known.ensure((size_t)std::max<int32_t>(G, 1)));
+    CK(ctx->d_seg_off.ensure((size_t)std::max<int32_t>(G, 1)));
+    SimParams p = params(ctx);
+    Ctl init{};
+    init.chunk_top = (unsigned long long)N;
+    init.arena_top = (unsigned long long)((ctx->prefix_total + 15) & ~15ll);
+    CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+    CK(cudaMemcpyAsync(ctx->d_ctl.p, &init, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_known.p, 0, sizeof(uint32_t) * std::max<int32_t>(G, 1), ctx->stream));
+    CK(cudaMemsetAsync(ctx->d_flag64.p, 0, sizeof(unsigned long long), ctx->stream));     // page iterator
+    const long long* in_off = ctx->window_active ? ctx->d_win_off.p : ctx->d_in_off.p;
+    CK(launch_init_given(p, in_off, ctx->stream));
+    CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+    CK(launch_csrp(p, ctx->d_pages.p, ctx->d_flag64.p, page_cap, L, ctx->d_first_page.p, ctx->d_known.p,
+                   ctx->d_out_cnt.p, in_off, threads, ctx->stream));
+    CK(cudaEventRecord(ctx->ev[2], ctx->stream));
+    unsigned long long pages_used = 0;
+    CK(cudaMemcpyAsync(&ctx->last, ctx->d_ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&pages_used, ctx->d_flag64.p, sizeof(pages_used), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const Ctl& c = ctx->last;
+    if (c.error & kErrArena)
+        return fail(ctx, GLS_ENOMEM, "CSRP store full: %llu pages of %u entries (raise the arena)", page_cap, L);
+    if (c.error & kErrDeep) return fail(ctx, GLS_ECUDA, "CSRP engine: a thread's individual memory overflowed");
+    // exact segments for the gate outputs, in net order after the given waveforms
+    std::vector<unsigned long long> cnt((size_t)std::max<int32_t>(G, 1)), off((size_t)std::max<int32_t>(G, 1));
+    if (G) CK(cudaMemcpy(cnt.data(), ctx->d_out_cnt.p + P, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost));
+    unsigned long long top = init.arena_top;
+    for (int32_t g = 0; g < G; ++g) {
+        off[g] = top;
+        top += (cnt[g] + 15) & ~15ull;
+    }
+    if (top > ctx->d_arena.n) return fail(ctx, GLS_ENOMEM, "arena too small for the collected result: %llu bytes",
+                                          top * 8ull);
+    if (G) CK(cudaMemcpyAsync(ctx->d_seg_off.p, off.data(), sizeof(unsigned long long) * G, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    CK(launch_csrp_collect(p, ctx->d_pages.p, L, ctx->d_first_page.p, ctx->d_out_cnt.p, ctx->d_seg_off.p,
+                           ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    float ms_k = 0, ms_s = 0;
+    cudaEventElapsedTime(&ms_k, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&ms_s, ctx->ev[0], ctx->ev[2]);
+    gls_stats& s = ctx->stats;
+    s = gls_stats{};
+    s.gate_evals = (int64_t)c.gate_evals;
+    s.events = (int64_t)c.events;
+    s.out_transitions = (int64_t)c.out_trans;
+    s.chunks = G;
+    s.levels = ctx->L;
+    s.arena_used_bytes = (int64_t)top * 8;
+    s.kernel_ms = ms_k;
+    s.simulate_ms = ms_s;
+    s.alg_bytes = -1;
+    s.csrp_pages = (int64_t)pages_used;
+    const int64_t given = ctx->window_active ? ctx->prefix_total - ((ctx->in_total + 15) & ~15ll) : ctx->in_total;
+    s.csrp_waste = (int64_t)pages_used * (int64_t)(L - 1) - (given + (int64_t)c.out_trans);
+    ctx->last_chunk_top = std::max<unsigned long long>(ctx->last_chunk_top, (unsigned long long)N);
+    ctx->has_result = true;
+    return GLS_OK;
 }
 
 int gls_get_stats(gls_ctx* ctx, gls_stats* out) {

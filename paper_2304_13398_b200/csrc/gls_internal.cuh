@@ -125,6 +125,15 @@ cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaS
 cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s);
 size_t warp_scratch_entries(int blocks);
 size_t warp_aux_bytes(int blocks);
+// engine 2 (CSRP pages + Alg. 1, gls_csrp.cuh)
+int csrp_coresident_threads(int device);
+size_t csrp_scratch_entries(int threads);
+cudaError_t launch_csrp(const SimParams& p, uint64_t* pages, unsigned long long* page_top,
+                        unsigned long long page_cap, uint32_t pagelen, unsigned long long* first_page,
+                        uint32_t* known, unsigned long long* out_cnt, const long long* in_off, int threads,
+                        cudaStream_t s);
+cudaError_t launch_csrp_collect(const SimParams& p, uint64_t* pages, uint32_t pagelen, unsigned long long* first_page,
+                                unsigned long long* out_cnt, const unsigned long long* seg_off, cudaStream_t s);
 int max_coresident_blocks(int device, int engine, int sched, int* per_sm);
 // time-window slice of the given waveforms (gls_simulate_window): per net the number of
 // kept entries, then the entries (collapse at t_clamp, keep t_clamp < t < t_end)

@@ -790,6 +790,10 @@ __device__ void chunk_done(const SimParams& p, unsigned long long id, const Chun
 }  // namespace gls
 #include "gls_lanes.cuh"
 namespace gls {
+constexpr int kCsrpStack = 1024;    // engine 2: a thread's individual memory (entries)
+}
+#include "gls_csrp.cuh"
+namespace gls {
 
 #ifndef GLS_MINB
 #define GLS_MINB 3
@@ -1132,6 +1136,44 @@ int max_coresident_blocks(int device, int engine, int sched, int* per_sm) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm) *per_sm = nb;
     return nb * sms;
+}
+
+
+// ---- engine 2 (the paper's CSRP store and Alg. 1, gls_csrp.cuh)
+constexpr int kCsrpThreads = 128;
+int csrp_coresident_threads(int device) {
+    int nb = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)cp::csrp_kernel, kCsrpThreads, 0);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    return nb * sms * kCsrpThreads;
+}
+size_t csrp_scratch_entries(int threads) { return (size_t)threads * kCsrpStack; }
+cudaError_t launch_csrp(const SimParams& p, uint64_t* pages, unsigned long long* page_top,
+                        unsigned long long page_cap, uint32_t pagelen, unsigned long long* first_page,
+                        uint32_t* known, unsigned long long* out_cnt, const long long* in_off, int threads,
+                        cudaStream_t s) {
+    cp::CsrpParams c{pages, page_top, page_cap, pagelen, first_page, known, out_cnt};
+    if (p.P > 0) {
+        int blocks = (p.P + 255) / 256;
+        if (blocks > 4096) blocks = 4096;
+        cp::csrp_given_kernel<<<blocks, 256, 0, s>>>(p, c, in_off);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (p.G == 0) return cudaSuccess;
+    SimParams q = p;
+    void* args[] = {&q, &c};
+    return cudaLaunchCooperativeKernel((const void*)cp::csrp_kernel, dim3(threads / kCsrpThreads), dim3(kCsrpThreads),
+                                       args, 0, s);
+}
+cudaError_t launch_csrp_collect(const SimParams& p, uint64_t* pages, uint32_t pagelen, unsigned long long* first_page,
+                                unsigned long long* out_cnt, const unsigned long long* seg_off, cudaStream_t s) {
+    if (p.G == 0) return cudaSuccess;
+    cp::CsrpParams c{pages, nullptr, 0, pagelen, first_page, nullptr, out_cnt};
+    long long blocks = ((long long)p.G + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    cp::csrp_collect_kernel<<<(unsigned)blocks, 256, 0, s>>>(p, c, seg_off);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s) {

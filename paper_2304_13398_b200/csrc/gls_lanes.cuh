@@ -67,6 +67,9 @@ constexpr float MINSPLIT = (float)GLS_MINSPLIT;  // split only a remainder of >=
 #define GLS_MAXSPLIT 8
 #endif
 constexpr int MAXSPLIT = GLS_MAXSPLIT;           // splits per re-balancing point
+#ifndef GLS_MINSLEEP
+#define GLS_MINSLEEP 64                          // ns: first back-off of a waiting warp
+#endif
 #ifndef GLS_MAXSLEEP
 #define GLS_MAXSLEEP 8192                        // ns: longest back-off of a warp waiting for published work
 #endif
@@ -187,6 +190,7 @@ struct Batch {
     int nun;                               // units (static + split)
     int8_t pend[32];                       // unit handed to a lane by a split (-1: none)
     uint32_t lev[32], levt[32];            // per-lane gate-evals / events of the batch
+    unsigned long long lcyc[32];           // per-lane clocks spent in unit set-up
     uint8_t sv_it[32];                     // (set-up call: the lane's round iteration,
     uint16_t sv_used[32];                  //  scratch fill)
     int8_t u_lnext[MAXU];                  // next unit taken by the same lane (-1: last)
@@ -524,6 +528,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
     B.pend[lane] = -1;
     B.lane_first[lane] = B.lane_last[lane] = -1;
     B.lev[lane] = B.levt[lane] = 0;
+    B.lcyc[lane] = 0;
     __syncwarp();
 
     for (;;) {
@@ -556,7 +561,9 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 B.sv_it[lane] = (uint8_t)it;
                 B.sv_used[lane] = (uint16_t)used;
                 UnitInit ui;                                             // (local memory: set-up path only)
+                const long long c_u0 = clock64();
                 const bool fast = unit_begin(p, u, ui);
+                B.lcyc[lane] += (unsigned long long)(clock64() - c_u0);
                 it = B.sv_it[lane];
                 used = B.sv_used[lane];
                 if (!fast) {                                             // long delays: per-lane ring engine
@@ -751,9 +758,11 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         __syncwarp();
     }
     const unsigned ev = __reduce_add_sync(FULL, B.lev[lane]), evt = __reduce_add_sync(FULL, B.levt[lane]);
+    const unsigned long long sc = warp_sum64(B.lcyc[lane]);
     if (lane == 0) {
         B.acc[A_EVALS] += ev;
         B.acc[A_EVENTS] += evt;
+        B.acc[A_CYC + 5] += sc / 32;                                     // (lane-average set-up clocks)
     }
     __syncwarp();
 }
@@ -815,7 +824,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
                     // wait for the claimed id to be published: poll its own ck_gate word
                     // (every waiting warp a different line); the shared completion count and
                     // error word only every 16th poll
-                    unsigned ns = 64, polls = 0;
+                    unsigned ns = GLS_MINSLEEP, polls = 0;
                     unsigned long long t_start = 0, seen = ~0ull;
                     for (;;) {
                         if (id < p.ck_cap) {
@@ -997,7 +1006,10 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         if (p.trace && lane == 0) {
             const unsigned long long d = gtimer() - B.c_t[j];
             atomicAdd(&p.trace[4ull * R.gi + 2], d);
-            atomicMax(&p.trace[4ull * R.gi + 3], d);
+            // (max duration in the low 44 bits, the batch's rounds and units above them)
+            atomicMax(&p.trace[4ull * R.gi + 3], ((unsigned long long)min(B.round, 4095) << 52) |
+                                                     ((unsigned long long)min(B.nun, 255) << 44) |
+                                                     min(d, (1ull << 44) - 1));
         }
         chunk_done<DATAFLOW>(p, id, R, B.acc);
     }

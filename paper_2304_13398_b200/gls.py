@@ -40,7 +40,8 @@ class gls_config(ctypes.Structure):
     _fields_ = [("arena_bytes", ctypes.c_int64), ("chunk_capacity", ctypes.c_int64),
                 ("chunk_events", ctypes.c_int32), ("blocks_per_sm", ctypes.c_int32),
                 ("ring_limit", ctypes.c_int32), ("engine", ctypes.c_int32), ("scheduler", ctypes.c_int32),
-                ("deep_per_warp", ctypes.c_int64), ("readback_mib", ctypes.c_int32), ("trace", ctypes.c_int32)]
+                ("deep_per_warp", ctypes.c_int64), ("readback_mib", ctypes.c_int32), ("trace", ctypes.c_int32),
+                ("csrp_pagelen", ctypes.c_int32)]
 
 
 class gls_cell_template(ctypes.Structure):
@@ -58,7 +59,7 @@ class gls_stats(ctypes.Structure):
                 ("lane_utilization", ctypes.c_double), ("batches", ctypes.c_int64),
                 ("batch_lanes", ctypes.c_double), ("batch_est", ctypes.c_double),
                 ("phase_cycles", ctypes.c_double * 6), ("balance", ctypes.c_double * 8),
-                ("kernel_ms", ctypes.c_double),
+                ("kernel_ms", ctypes.c_double), ("csrp_pages", ctypes.c_int64), ("csrp_waste", ctypes.c_int64),
                 ("simulate_ms", ctypes.c_double)]
 
     def as_dict(self):
@@ -179,9 +180,9 @@ class Context:
 
     # ---- ABI calls ----------------------------------------------------------
     def gls_set_config(self, arena_bytes=0, chunk_capacity=0, chunk_events=0, blocks_per_sm=0, ring_limit=0,
-                       engine=0, scheduler=0, deep_per_warp=0, readback_mib=0, trace=0):
+                       engine=0, scheduler=0, deep_per_warp=0, readback_mib=0, trace=0, csrp_pagelen=0):
         c = gls_config(arena_bytes, chunk_capacity, chunk_events, blocks_per_sm, ring_limit, engine, scheduler,
-                       deep_per_warp, readback_mib, trace)
+                       deep_per_warp, readback_mib, trace, csrp_pagelen)
         return self._check(self._lib.gls_set_config(self._h, ctypes.byref(c)))
 
     def gls_load_netlist(self, num_inputs, gate_type, fanin_offsets, fanin_net, pin_delay):

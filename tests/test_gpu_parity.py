@@ -29,6 +29,9 @@ def run_oracle(nl, st, dur):
 # scheduler 0 = dataflow (default), 1 = level barriers
 ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1)]
 EIDS = ["units-df", "units-lvl", "lane"]
+# engine 2 = the paper's CSRP pages + Alg. 1 (A/B baseline), small page lengths included
+CSRP = [dict(engine=2), dict(engine=2, csrp_pagelen=2), dict(engine=2, csrp_pagelen=7)]
+CIDS = ["csrp256", "csrp2", "csrp7"]
 
 
 def run_gpu(c, nl, st, dur, **cfg):
@@ -412,3 +415,44 @@ def test_window_stitch_over_nccl_single_rank(ctx):
     finally:
         dist.destroy_process_group()
     assert np.array_equal(h.cpu().numpy().view(np.uint64), ctx.gls_get_net_hashes())
+
+
+@pytest.mark.parametrize("engine", CSRP, ids=CIDS)
+def test_csrp_engine_parity(ctx, engine):
+    """NEXT-3: the paper's design on the GPU — CSRP pages, next-page pointers, terminate
+    markers, an atomic page iterator (§3.1) and Alg. 1's static one-thread-
+    per-cell assignment — bit-exact against the oracle, with Eq. 4's waste bound
+    M_w <= pagelen * k * M_t on the page slots."""
+    rng = np.random.Generator(np.random.PCG64(77))
+    for d in range(120):
+        P = int(rng.integers(1, 10))
+        nl = W.random_dag(20_000 + d, P, int(rng.integers(1, 150)), max_delay=int(rng.integers(0, 15)))
+        st = W.random_stimuli(d, P, int(rng.integers(0, 60)), 400, xz=float(rng.random() * 0.3),
+                              max_gap=int(rng.integers(1, 30)))
+        s = assert_same(ctx, nl, st, 450, hashes=(d % 10 == 0), **engine)
+        L = engine.get("csrp_pagelen", 256)
+        k = nl.num_nets
+        assert 0 <= s["csrp_waste"] <= L * k
+        assert s["csrp_pages"] >= k
+    for ex in golden_io.examples():
+        nl, st, dur, index, exp = ex.build()
+        w, _ = run_gpu(ctx, nl, st, dur, **engine)
+        for net, wave in exp.items():
+            assert w.wave(net) == wave, (ex.name, nl.names[net])
+
+
+def test_csrp_engine_c7552_and_cells(ctx):
+    nl = W.config_netlist("c7552")
+    spec = W.config_stimspec("c7552")
+    o, t = W.generate_stimuli(spec)
+    st = W.Stimuli(o.numpy(), t.numpy().astype(np.uint64))
+    assert_same(ctx, nl, st, spec.duration, engine=2)
+    tpl, ct, cf, cd = W.random_cells(91, 6, 120, max_delay=12, p_inf=0.2)
+    st = W.random_stimuli(91, 6, 80, 2000, xz=0.1)
+    ref = oracle.simulate_cells(6, tpl, ct, cf, cd, st.offsets, st.trans, 2100)
+    ctx.gls_set_config(engine=2)
+    ctx.gls_load_cells(6, tpl, ct, cf, cd)
+    ctx.gls_set_input_waveforms(6, st.offsets, st.trans)
+    ctx.gls_simulate(2100)
+    w = ctx.gls_get_waveforms()
+    assert np.array_equal(w.offsets, ref.offsets) and np.array_equal(w.trans, ref.trans)
