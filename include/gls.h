@@ -319,10 +319,12 @@ int gls_get_stats(gls_ctx *ctx, gls_stats *out);
  * that makes a time window exact (reading R17).  Needs a netlist. */
 int gls_get_halo(gls_ctx *ctx, int64_t *halo_ps);
 /* Scheduling trace of the last gls_simulate run with gls_config.trace = 1 (diagnostics,
- * SURVEY §5 tracing): host uint64 [4 * num_gates], per gate in the caller's order:
- * %globaltimer ns when the gate was planned (its chunks published, Alg. 1's unlock),
- * when its last chunk completed, the sum and the maximum of its chunks' durations
- * (claim to completion, ns).  GLS_ESTATE without a traced result. */
+ * SURVEY §5 tracing): host uint64 [8 * num_gates], per gate in the caller's order:
+ * [0] %globaltimer ns when the gate was planned (its chunks published, Alg. 1's unlock),
+ * [1] when its last chunk completed, [2] the sum and [3] the maximum of its chunks'
+ * durations (claim to completion, ns); for the batch of the slowest chunk (engine 0):
+ * [4] re-balancing rounds, [5] units, [6] the busiest lane's iterations, [7] the most unit
+ * set-ups of one lane.  GLS_ESTATE without a traced result. */
 int gls_get_trace(gls_ctx *ctx, uint64_t *trace);
 /* Number of topological levels of the loaded netlist (0 without gates). */
 int gls_get_levels(gls_ctx *ctx, int32_t *levels);

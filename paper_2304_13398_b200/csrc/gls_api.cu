@@ -910,8 +910,8 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
         init.arena_top = (unsigned long long)((ctx->prefix_total + 15) & ~15ll);   // 128-byte segments
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         if (ctx->cfg.trace) {
-            CK(ctx->d_trace.ensure((size_t)4 * std::max<int32_t>(ctx->G, 1)));
-            CK(cudaMemsetAsync(ctx->d_trace.p, 0, sizeof(unsigned long long) * 4 * std::max<int32_t>(ctx->G, 1),
+            CK(ctx->d_trace.ensure((size_t)8 * std::max<int32_t>(ctx->G, 1)));
+            CK(cudaMemsetAsync(ctx->d_trace.p, 0, sizeof(unsigned long long) * 8 * std::max<int32_t>(ctx->G, 1),
                                ctx->stream));
             p.trace = ctx->d_trace.p;
         }
@@ -1105,10 +1105,10 @@ int gls_get_stats(gls_ctx* ctx, gls_stats* out) {
 int gls_get_trace(gls_ctx* ctx, uint64_t* trace) {
     if (!ctx || !trace) return GLS_EINVAL;
     if (!ctx->has_result || !ctx->traced) return fail(ctx, GLS_ESTATE, "no traced simulation result (gls_config.trace)");
-    std::vector<unsigned long long> t((size_t)4 * ctx->G);
-    if (ctx->G) CK(cudaMemcpy(t.data(), ctx->d_trace.p, sizeof(unsigned long long) * 4 * ctx->G, cudaMemcpyDeviceToHost));
+    std::vector<unsigned long long> t((size_t)8 * ctx->G);
+    if (ctx->G) CK(cudaMemcpy(t.data(), ctx->d_trace.p, sizeof(unsigned long long) * 8 * ctx->G, cudaMemcpyDeviceToHost));
     for (int32_t g = 0; g < ctx->G; ++g)
-        for (int q = 0; q < 4; ++q) trace[4ll * g + q] = t[4ll * ctx->inv[g] + q];
+        for (int q = 0; q < 8; ++q) trace[8ll * g + q] = t[8ll * ctx->inv[g] + q];
     return GLS_OK;
 }
 

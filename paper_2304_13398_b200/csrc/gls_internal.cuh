@@ -117,7 +117,7 @@ struct SimParams {
     int32_t engine;             // 0 = lanes on re-balanced units, 1 = per-lane chunks
     int32_t sched;              // 0 = dataflow (ready counters), 1 = level barriers
     uint32_t nblocks;
-    unsigned long long* trace;  // [4 G] or null: plan time, completion time, Σ / max chunk durations (ns)
+    unsigned long long* trace;  // [8 G] or null (gls_get_trace)
 };
 
 // kernels / launchers (gls_kernels.cu)

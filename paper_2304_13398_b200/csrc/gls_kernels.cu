@@ -688,7 +688,7 @@ __device__ void plan_gate(const SimParams& p, uint32_t c) {
         return;
     }
     if (lane == 0) {
-        if (p.trace) p.trace[4ull * c] = gtimer();
+        if (p.trace) p.trace[8ull * c] = gtimer();
         p.net_ck[p.P + c] = (uint32_t)base;
         p.net_nck[p.P + c] = (uint32_t)nch;
         p.gate_nin[c] = n_in;
@@ -725,7 +725,7 @@ __device__ void gate_complete(const SimParams& p, uint32_t gi, uint32_t base, ui
     }
     if (lane == 0) {
         p.net_len[p.P + gi] = cum;
-        if (p.trace) p.trace[4ull * gi + 1] = gtimer();
+        if (p.trace) p.trace[8ull * gi + 1] = gtimer();
     }
     if (!DATAFLOW) return;
     fence_release();

@@ -42,7 +42,7 @@ constexpr uint32_t kRebaseQ = 0x80000000u;       // entry form of t - B = 2^29
 constexpr uint32_t kFastDelay = 0xFFFFu;         // gates with dmax below this use the 32-bit sweep (u16 delays;
                                                  // 0xFFFF there = GLS_DELAY_INF)
 #ifndef GLS_LCAP
-#define GLS_LCAP 4096
+#define GLS_LCAP 8192
 #endif
 constexpr int LCAP = GLS_LCAP;                   // per-lane output scratch (stack) entries
 constexpr unsigned long long U_MAX = LCAP / 4;   // most expected entries of a static unit
@@ -59,6 +59,9 @@ constexpr int W_MIN = GLS_WMIN;                  // fewest expected entries per 
 #define GLS_ROUND 32
 #endif
 constexpr int ROUND = GLS_ROUND;                 // sweep iterations between re-balancing points
+#ifndef GLS_MQ_MIN
+#define GLS_MQ_MIN 0                             // chunks with at least this many expected entries are
+#endif                                           // sliced at merged-count quantiles (0: never)
 #ifndef GLS_MINSPLIT
 #define GLS_MINSPLIT 64
 #endif
@@ -191,6 +194,7 @@ struct Batch {
     int8_t pend[32];                       // unit handed to a lane by a split (-1: none)
     uint32_t lev[32], levt[32];            // per-lane gate-evals / events of the batch
     unsigned long long lcyc[32];           // per-lane clocks spent in unit set-up
+    uint32_t lit[32], lsu[32];             // per-lane iterations / unit set-ups of the batch (trace)
     uint8_t sv_it[32];                     // (set-up call: the lane's round iteration,
     uint16_t sv_used[32];                  //  scratch fill)
     int8_t u_lnext[MAXU];                  // next unit taken by the same lane (-1: last)
@@ -374,6 +378,54 @@ __device__ __forceinline__ void locate_all(const SimParams& p, const uint32_t* s
     }
 }
 
+// Number of entries before time T summed over the k pins' nets (count_before of
+// gls_kernels.cu for all pins at once, the binary searches in lockstep).
+__device__ unsigned long long count_before_all(const SimParams& p, const uint32_t* src, uint32_t k, long long T) {
+    uint32_t cb[4], lo[4], hi[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        cb[i] = (uint32_t)i < k ? __ldcg(&p.net_ck[src[i]]) : 0u;
+        lo[i] = 0;
+        hi[i] = (uint32_t)i < k ? __ldcg(&p.net_nck[src[i]]) : 1u;
+    }
+    for (;;) {                                      // largest j with ck_T[j] <= T (default 0)
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (hi[i] - lo[i] > 1) {
+                any = true;
+                const uint32_t mid = (lo[i] + hi[i]) >> 1;
+                if (__ldcg(&p.ck_T[cb[i] + mid]) <= T) lo[i] = mid; else hi[i] = mid;
+            }
+        }
+        if (!any) break;
+    }
+    const uint64_t* seg[4];
+    uint32_t a[4], b[4];
+    unsigned long long base = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t j = cb[i] + lo[i];
+        seg[i] = (uint32_t)i < k ? p.arena + __ldcg(&p.ck_off[j]) : p.arena;
+        a[i] = 0;
+        b[i] = (uint32_t)i < k ? __ldcg(&p.ck_cnt[j]) : 0u;
+        base += (uint32_t)i < k ? __ldcg(&p.ck_cum[j]) : 0ull;
+    }
+    for (;;) {                                      // first index with t >= T
+        bool any = false;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            if (a[i] < b[i]) {
+                any = true;
+                const uint32_t m = (a[i] + b[i]) >> 1;
+                if (etime(seg[i][m]) < T) a[i] = m + 1; else b[i] = m;
+            }
+        }
+        if (!any) break;
+    }
+    return base + a[0] + a[1] + a[2] + a[3];
+}
+
 // Start unit u on this lane (the set-up path, kept out of the sweep's registers):
 // its delay table, the cursors of its pins at tau0 = T0 - dmax - 1 (binary search over
 // chunk start times, then inside the segment; value in effect from ck_vb), the first
@@ -529,6 +581,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
     B.lane_first[lane] = B.lane_last[lane] = -1;
     B.lev[lane] = B.levt[lane] = 0;
     B.lcyc[lane] = 0;
+    B.lit[lane] = B.lsu[lane] = 0;
     __syncwarp();
 
     for (;;) {
@@ -556,6 +609,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 // nothing but constants lives across the set-up call: the round's counts, the
                 // iteration and the scratch fill go through shared memory (set-up path only)
                 B.lev[lane] += l_cnt & 0xffffu;
+            B.lit[lane] += (uint32_t)it;
                 B.levt[lane] += l_cnt >> 16;
                 l_cnt = 0;
                 B.sv_it[lane] = (uint8_t)it;
@@ -564,6 +618,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 const long long c_u0 = clock64();
                 const bool fast = unit_begin(p, u, ui);
                 B.lcyc[lane] += (unsigned long long)(clock64() - c_u0);
+                B.lsu[lane] += 1;
                 it = B.sv_it[lane];
                 used = B.sv_used[lane];
                 if (!fast) {                                             // long delays: per-lane ring engine
@@ -693,6 +748,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         {
             const unsigned itmax = __reduce_max_sync(FULL, (unsigned)it), itsum = __reduce_add_sync(FULL, (unsigned)it);
             B.lev[lane] += l_cnt & 0xffffu;
+            B.lit[lane] += (uint32_t)it;
             B.levt[lane] += l_cnt >> 16;
             l_cnt = 0;
             if (lane == 0) {
@@ -727,7 +783,9 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 ts = tn + (T1u - tn) / 2;                                 // > every timestamp applied so far
             }
         }
-        unsigned rcv = idle;
+        // (a lane whose scratch is half full takes no split: the units it already holds keep
+        // their room, and no unit ends in the slow fallback for want of it)
+        unsigned rcv = idle & __ballot_sync(FULL, used < (uint32_t)LCAP / 2);
         int nun = B.nun;
         for (int q = 0; q < MAXSPLIT && rcv && nun < MAXU; ++q) {
             const unsigned mx = __reduce_max_sync(FULL, __float_as_uint(re));   // re >= 0: bits order like values
@@ -923,6 +981,33 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         if (q == 0) B.c_T0[j] = s.T0;
     }
     __syncwarp();
+#if GLS_MQ_MIN > 0
+    // big chunks: slices at quantiles of the MERGED input count instead (what a lane's work
+    // is), found warp-cooperatively — lane l takes the candidate time t_l at the l/32
+    // quantile of the longest fan-in and counts all k fan-ins' entries before it (binary
+    // searches in lockstep); boundary s is the latest candidate whose merged count is at
+    // most s/ns of the chunk's
+    for (int j = 0; j < nc; ++j) {
+        const int ns = B.c_nsl[j];
+        if (ns <= 1 || B.u_est[B.c_first[j]] * (unsigned)ns < (unsigned)GLS_MQ_MIN) continue;
+        ChunkSetup s;
+        uint32_t gi, cidx, nch, ref;
+        unsigned long long q0, q1, nin;
+        setup_chunk(p, B.id[j], s, gi, cidx, nch, &q0, &q1, &ref, &nin);
+        const long long t = lane == 0 ? s.T0 : time_at(p, ref, q0 + ((q1 - q0) * (unsigned long long)lane) / 32ull);
+        const unsigned long long mc = count_before_all(p, s.src, s.k, t);
+        const unsigned long long m1 = lane == 0 ? count_before_all(p, s.src, s.k, s.T1) : 0ull;
+        const unsigned long long m0 = __shfl_sync(FULL, mc, 0), me = __shfl_sync(FULL, m1, 0);
+        const int f = B.c_first[j];
+        for (int q = 1; q < ns; ++q) {
+            const unsigned long long target = m0 + (me - m0) * (unsigned long long)q / (unsigned long long)ns;
+            const unsigned bal = __ballot_sync(FULL, mc <= target);
+            const long long tq = __shfl_sync(FULL, t, 31 - __clz(bal));
+            if (lane == 0) B.u_T0[f + q] = tq;
+        }
+    }
+    __syncwarp();
+#endif
     for (int u = lane; u < nstatic; u += 32)
         if (B.u_next[u] != kEnd) B.u_T1[u] = B.u_T0[u + 1];
     __syncwarp();
@@ -990,6 +1075,11 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
     }
     __syncwarp();
     const long long c_out = clock64();
+    unsigned long long t_maxit = 0, t_maxsu = 0;
+    if (p.trace) {
+        t_maxit = __reduce_max_sync(FULL, B.lit[lane]);
+        t_maxsu = __reduce_max_sync(FULL, B.lsu[lane]);
+    }
     // ---- complete the chunks (whole warp, one after the other)
     for (int j = 0; j < nc; ++j) {
         const unsigned long long id = B.id[j];
@@ -1005,11 +1095,14 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         R.events = 0;
         if (p.trace && lane == 0) {
             const unsigned long long d = gtimer() - B.c_t[j];
-            atomicAdd(&p.trace[4ull * R.gi + 2], d);
-            // (max duration in the low 44 bits, the batch's rounds and units above them)
-            atomicMax(&p.trace[4ull * R.gi + 3], ((unsigned long long)min(B.round, 4095) << 52) |
-                                                     ((unsigned long long)min(B.nun, 255) << 44) |
-                                                     min(d, (1ull << 44) - 1));
+            unsigned long long* tr = p.trace + 8ull * R.gi;
+            atomicAdd(&tr[2], d);
+            if (atomicMax(&tr[3], d) < d) {                 // the slowest chunk's batch (racy only across chunks)
+                tr[4] = (unsigned long long)B.round;
+                tr[5] = (unsigned long long)B.nun;
+                tr[6] = t_maxit;
+                tr[7] = t_maxsu;
+            }
         }
         chunk_done<DATAFLOW>(p, id, R, B.acc);
     }

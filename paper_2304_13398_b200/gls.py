@@ -295,7 +295,7 @@ class Context:
         return s.as_dict()
 
     def gls_get_trace(self) -> np.ndarray:
-        t = np.zeros((self.num_gates, 4), np.uint64)
+        t = np.zeros((self.num_gates, 8), np.uint64)
         self._check(self._lib.gls_get_trace(self._h, t.ctypes.data))
         return t
 

@@ -37,10 +37,8 @@ glev = lev[P:]
 t0 = tr[:, 0][tr[:, 0] > 0].min()
 plan, done = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3          # us
 csum = tr[:, 2] / 1e3
-t3 = ctx.gls_get_trace()[:, 3]
-cmax = (t3 & np.uint64((1 << 44) - 1)).astype(np.float64) / 1e3
-crounds = (t3 >> np.uint64(52)).astype(np.int64)
-cunits = ((t3 >> np.uint64(44)) & np.uint64(255)).astype(np.int64)
+cmax = tr[:, 3] / 1e3
+crounds, cunits, cmaxit, cmaxsu = (tr[:, q].astype(np.int64) for q in (4, 5, 6, 7))
 n_in = np.zeros(G)
 counts = ctx.gls_get_net_counts()
 for g in range(G):
@@ -65,4 +63,4 @@ slow = np.argsort(-cmax)[:10]
 for g in slow:
     print(f"slowest chunk: gate {g} level {glev[g]} n_in {n_in[g]:.0f} max chunk {cmax[g]:.0f} us, "
           f"sum {csum[g]:.0f} us, planned {plan[g]:.0f} us, done {done[g]:.0f} us, batch rounds {crounds[g]} "
-          f"units {cunits[g]}")
+          f"units {cunits[g]} busiest lane {cmaxit[g]} iterations, most set-ups {cmaxsu[g]}")
