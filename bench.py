@@ -204,7 +204,8 @@ def balance_str(s):
     b = s.get("balance") or [0] * 8
     nb = max(1, s.get("batches") or 1)
     return (f"[units/batch {b[0] / nb:.1f}, splits/batch {b[1] / nb:.2f}, rounds/batch {b[2] / nb:.1f}, "
-            f"fallback units {int(b[3])}]")
+            f"fallback units {int(b[3])}, set-up/end/re-balance clocks of the sweep "
+            f"{[round(x / max(1.0, (s.get('phase_cycles') or [0] * 6)[2]), 3) for x in b[4:7]]}]")
 
 
 def post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_hashes, stims):

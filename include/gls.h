@@ -129,7 +129,9 @@ typedef struct gls_stats {
                                 lane-average clocks in unit set-up (part of the sweep) */
     double balance[8];       /* engine 0 counters: [0] static units, [1] units split off
                                 while running, [2] re-balancing rounds, [3] fallback
-                                units (per-lane ring engine), [4]-[7] unused          */
+                                units (per-lane ring engine); warp-level clocks (lane
+                                0, summed over warps) in [4] unit set-up passes, [5]
+                                unit-end passes, [6] re-balancing points; [7] unused  */
     double kernel_ms;        /* CUDA-event time of the gate-evaluation kernel      */
     int64_t csrp_pages;      /* engine 2: CSRP pages handed out                     */
     int64_t csrp_waste;      /* engine 2: page slots not holding an entry (Eq. 4 bounds

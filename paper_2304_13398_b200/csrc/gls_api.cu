@@ -1018,13 +1018,20 @@ static int simulate_csrp(gls_ctx* ctx, int64_t duration) {
     const int64_t fit = (int64_t)(0.45 * (double)free_bytes(ctx)) / (8 * (int64_t)L);
     want = std::max<int64_t>(16, std::min(want, fit));
     if ((int64_t)ctx->d_pages.n < want * (int64_t)L) CK(ctx->d_pages.alloc((size_t)want * L));
-    const unsigned long long page_cap = ctx->d_pages.n / L;
     CK(ctx->d_first_page.ensure((size_t)N + 1));
     CK(ctx->d_out_cnt.ensure((size_t)N + 1));
     CK(ctx->d_known.ensure((size_t)std::max<int32_t>(G, 1)));
     CK(ctx->d_seg_off.ensure((size_t)std::max<int32_t>(G, 1)));
-    SimParams p = params(ctx);
+    const bool auto_size = ctx->cfg.arena_bytes == 0;
     Ctl init{};
+    unsigned long long top = 0, pages_used = 0;
+    std::vector<unsigned long long> cnt((size_t)std::max<int32_t>(G, 1)), off((size_t)std::max<int32_t>(G, 1));
+    // (auto-sized store: a full page store grows once to the largest that fits, and the arena
+    // to what the collected result needs, then the run is repeated)
+    for (int attempt = 0;; ++attempt) {
+    const unsigned long long page_cap = ctx->d_pages.n / L;
+    SimParams p = params(ctx);
+    init = Ctl{};
     init.chunk_top = (unsigned long long)N;
     init.arena_top = (unsigned long long)((ctx->prefix_total + 15) & ~15ll);
     CK(cudaEventRecord(ctx->ev[0], ctx->stream));
@@ -1037,24 +1044,41 @@ static int simulate_csrp(gls_ctx* ctx, int64_t duration) {
     CK(launch_csrp(p, ctx->d_pages.p, ctx->d_flag64.p, page_cap, L, ctx->d_first_page.p, ctx->d_known.p,
                    ctx->d_out_cnt.p, in_off, threads, ctx->stream));
     CK(cudaEventRecord(ctx->ev[2], ctx->stream));
-    unsigned long long pages_used = 0;
     CK(cudaMemcpyAsync(&ctx->last, ctx->d_ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaMemcpyAsync(&pages_used, ctx->d_flag64.p, sizeof(pages_used), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     const Ctl& c = ctx->last;
-    if (c.error & kErrArena)
-        return fail(ctx, GLS_ENOMEM, "CSRP store full: %llu pages of %u entries (raise the arena)", page_cap, L);
     if (c.error & kErrDeep) return fail(ctx, GLS_ECUDA, "CSRP engine: a thread's individual memory overflowed");
+    if (c.error & kErrArena) {
+        if (auto_size && attempt == 0) {
+            const int64_t most = (int64_t)(0.45 * (double)(free_bytes(ctx) + 8 * ctx->d_pages.n)) / (8 * (int64_t)L);
+            if (most > (int64_t)page_cap) {
+                ctx->d_pages.release();
+                CK(ctx->d_pages.alloc((size_t)most * L));
+                continue;
+            }
+        }
+        return fail(ctx, GLS_ENOMEM, "CSRP store full: %llu pages of %u entries (raise the arena)", page_cap, L);
+    }
     // exact segments for the gate outputs, in net order after the given waveforms
-    std::vector<unsigned long long> cnt((size_t)std::max<int32_t>(G, 1)), off((size_t)std::max<int32_t>(G, 1));
     if (G) CK(cudaMemcpy(cnt.data(), ctx->d_out_cnt.p + P, sizeof(unsigned long long) * G, cudaMemcpyDeviceToHost));
-    unsigned long long top = init.arena_top;
+    top = init.arena_top;
     for (int32_t g = 0; g < G; ++g) {
         off[g] = top;
         top += (cnt[g] + 15) & ~15ull;
     }
-    if (top > ctx->d_arena.n) return fail(ctx, GLS_ENOMEM, "arena too small for the collected result: %llu bytes",
-                                          top * 8ull);
+    if (top > ctx->d_arena.n) {
+        if (auto_size && attempt < 2) {
+            const int rc2 = ensure_arena(ctx, (int64_t)top + 1, false);
+            if (rc2) return rc2;
+            continue;                                  // (pages are intact, but re-run: simplest exact path)
+        }
+        return fail(ctx, GLS_ENOMEM, "arena too small for the collected result: %llu bytes", top * 8ull);
+    }
+    break;
+    }
+    SimParams p = params(ctx);
+    const Ctl& c = ctx->last;
     if (G) CK(cudaMemcpyAsync(ctx->d_seg_off.p, off.data(), sizeof(unsigned long long) * G, cudaMemcpyHostToDevice,
                               ctx->stream));
     CK(launch_csrp_collect(p, ctx->d_pages.p, L, ctx->d_first_page.p, ctx->d_out_cnt.p, ctx->d_seg_off.p,

@@ -617,7 +617,11 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 UnitInit ui;                                             // (local memory: set-up path only)
                 const long long c_u0 = clock64();
                 const bool fast = unit_begin(p, u, ui);
-                B.lcyc[lane] += (unsigned long long)(clock64() - c_u0);
+                {
+                    const unsigned long long dc = (unsigned long long)(clock64() - c_u0);
+                    B.lcyc[lane] += dc;
+                    if (lane == __ffs(__activemask()) - 1) B.acc[A_BAL + 4] += dc;   // warp-level: one pass
+                }
                 B.lsu[lane] += 1;
                 it = B.sv_it[lane];
                 used = B.sv_used[lane];
@@ -665,7 +669,9 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 }
                 // ---- unit done: its outputs are the stack entries in [T0, min(T1, duration + 1))
                 cp_wait<0>();                                            // no copy may land in the next unit's cursors
+                const long long c_e0 = clock64();
                 unit_end(p, B, u, sbase, n, used, l_cnt);
+                if (lane == __ffs(__activemask()) - 1) B.acc[A_BAL + 5] += (unsigned long long)(clock64() - c_e0);
                 u = -1;
                 continue;
             } else {
@@ -745,6 +751,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         }
         // ---- re-balancing point
         __syncwarp();
+        const long long c_rb = clock64();
         {
             const unsigned itmax = __reduce_max_sync(FULL, (unsigned)it), itsum = __reduce_add_sync(FULL, (unsigned)it);
             B.lev[lane] += l_cnt & 0xffffu;
@@ -812,7 +819,10 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
             if (lane == 0) B.acc[A_BAL + 1] += 1ull;
         }
         __syncwarp();
-        if (lane == 0) B.nun = nun;
+        if (lane == 0) {
+            B.nun = nun;
+            B.acc[A_BAL + 6] += (unsigned long long)(clock64() - c_rb);
+        }
         __syncwarp();
     }
     const unsigned ev = __reduce_add_sync(FULL, B.lev[lane]), evt = __reduce_add_sync(FULL, B.levt[lane]);

@@ -456,3 +456,34 @@ def test_csrp_engine_c7552_and_cells(ctx):
     ctx.gls_simulate(2100)
     w = ctx.gls_get_waveforms()
     assert np.array_equal(w.offsets, ref.offsets) and np.array_equal(w.trans, ref.trans)
+
+
+def test_deep_scratch_retry_on_fresh_context():
+    """kErrDeep grow-and-retry: a fresh context with a 1-entry deep scratch per warp and a
+    1-entry pending ring (per-lane engine) must overflow the deep scratch, grow it and
+    still return the oracle's result; deep_per_warp set after a first run takes effect."""
+    nl = W.random_dag(1400, 5, 60, max_delay=40)
+    st = W.random_stimuli(3, 5, 80, 800, xz=0.2, max_gap=4)
+    ref = run_oracle(nl, st, 900)
+    with gls.Context(0) as c:
+        s = assert_same(c, nl, st, 900, ref=ref, engine=1, ring_limit=1, chunk_events=9, deep_per_warp=1)
+        assert s["deep_chunks"] > 0
+        s = assert_same(c, nl, st, 900, ref=ref, engine=0, deep_per_warp=1)
+        s = assert_same(c, nl, st, 900, ref=ref, engine=1, ring_limit=1, chunk_events=9, deep_per_warp=2)
+
+
+def test_auto_arena_regrow():
+    """Auto-sized transition store (arena_bytes = 0) smaller than the result: an XOR ladder
+    (net k = XOR(net k-2, net k-1)) whose activity grows along the chain outruns the size
+    estimate; the kernel aborts, the store grows (given waveforms kept) and the retried run
+    equals the oracle."""
+    G = 30
+    nl = W.netlist_from_gates(2, [(W.XOR, [g, g + 1], [(1, 1, 1, 1)] * 2) for g in range(G)])
+    waves = [[(97 * j + 3, j % 2) for j in range(1, 300)], [(131 * j + 5, j % 2) for j in range(1, 200)]]
+    st = W.stimuli_from_lists(waves)
+    ref = run_oracle(nl, st, 100000)
+    est = st.total + 3 * G * (st.total // 2) + 4096   # gls_api.cu ensure_arena's auto estimate
+    assert ref.out_trans > est                        # so the retry path runs
+    with gls.Context(0) as c:
+        for eng in (0, 1, 2):
+            assert_same(c, nl, st, 100000, ref=ref, engine=eng)
