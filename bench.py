@@ -58,6 +58,10 @@ def parse():
     ap.add_argument("--arena-gb", type=float, default=0.0)
     ap.add_argument("--engine", type=int, default=0)
     ap.add_argument("--scheduler", type=int, default=0)
+    ap.add_argument("--ncycles", type=int, default=0,
+                    help="A/B / profiling only: override the config's number of clock cycles")
+    ap.add_argument("--wcv", type=float, default=0.0,
+                    help="A/B only: override the skewed profile's WCV target (Eq. 5) of the config")
     return ap.parse_args()
 
 
@@ -486,7 +490,8 @@ def run_gls(a):
             "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": cfg, "gates": nl.num_gates, "pis": nl.num_inputs, "pins": nl.num_pins,
+            "config": {"workload": cfg + (f"@wcv{a.wcv:g}" if a.wcv > 0 else "") + (f"@{a.ncycles}cyc" if a.ncycles > 0 else ""), "gates": nl.num_gates,
+                       "pis": nl.num_inputs, "pins": nl.num_pins,
                        "levels": L, "duration_ps": spec.duration, "stimulus_transitions": n_in,
                        "stimulus_wcv": round(wcv, 2), "halo_ps": H,
                        **({"stimulus_sets": C5_SETS, "sets_per_rank": len(stims),
@@ -514,6 +519,11 @@ def run_gls(a):
 
 def main():
     a = parse()
+    if a.wcv > 0:                          # (A/B of the kernel across input skew; not a bench line)
+        W.CONFIGS[a.config] = dict(W.CONFIGS[a.config], profile="skewed", wcv=a.wcv,
+                                   mean_trans=W.CONFIGS[a.config].get("mean_trans") or 1000)
+    if a.ncycles > 0:
+        W.CONFIGS[a.config] = dict(W.CONFIGS[a.config], ncycles=a.ncycles)
     if a.impl == "reference":
         return run_reference(a)
     return run_gls(a)

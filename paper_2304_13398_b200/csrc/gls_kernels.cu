@@ -1132,6 +1132,19 @@ int max_coresident_blocks(int device, int engine, int sched, int* per_sm) {
     int nb = 0, sms = 0;
     const void* k = kernel_for(engine, sched);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem(engine));
+    // shared-memory carveout: just what the resident CTAs need (the rest stays L1, which
+    // caches the fan-in entries the sweep reads: engine 0 at 3 CTAs/SM keeps ~92 KB)
+    if (engine == 0) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, k);
+        int maxsm = 0, want = 3;
+        cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+        const size_t per = fa.sharedSizeBytes + dyn_smem(engine) + 1024;      // + the per-CTA reservation
+        if (maxsm > 0) {
+            const int pct = (int)((want * per * 100 + (size_t)maxsm - 1) / (size_t)maxsm);
+            cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+        }
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kThreads, dyn_smem(engine));
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     if (per_sm) *per_sm = nb;

@@ -181,10 +181,7 @@ struct Batch {
     uint32_t c_total[MAXC];
     uint8_t c_first[MAXC], c_nsl[MAXC];    // first unit, static slices
     uint8_t c_inf[MAXC];                   // the chunk's gate has a GLS_DELAY_INF pin: one unit, never split
-    unsigned long long c_t[MAXC];          // claim time (gls_config.trace)
     long long u_T0[MAXU], u_T1[MAXU];      // unit time range
-    uint32_t u_soff[MAXU], u_cnt[MAXU];    // outputs: lane-scratch offset, count
-    uint32_t u_pre[MAXU];                  // offset of the unit's outputs inside its chunk
     uint32_t u_est[MAXU];                  // expected merged entries
     uint8_t u_chunk[MAXU], u_slice[MAXU], u_lane[MAXU], u_vb[MAXU], u_st[MAXU], u_next[MAXU];
     int qhead;                             // next static unit to hand out
@@ -193,8 +190,6 @@ struct Batch {
     int nun;                               // units (static + split)
     int8_t pend[32];                       // unit handed to a lane by a split (-1: none)
     uint32_t lev[32], levt[32];            // per-lane gate-evals / events of the batch
-    unsigned long long lcyc[32];           // per-lane clocks spent in unit set-up
-    uint32_t lit[32], lsu[32];             // per-lane iterations / unit set-ups of the batch (trace)
     uint8_t sv_it[32];                     // (set-up call: the lane's round iteration,
     uint16_t sv_used[32];                  //  scratch fill)
     int8_t u_lnext[MAXU];                  // next unit taken by the same lane (-1: last)
@@ -206,15 +201,28 @@ constexpr size_t kBatchBytes = (sizeof(Batch) + 15) & ~(size_t)15;
 struct WarpAux {
     uint32_t u_deep[MAXU];                 // fallback: deep-ring offset in the warp's region (~0: none)
     uint32_t u_sev[MAXU], u_sevt[MAXU];    // the lane's counts when the unit started
+    // unit outputs: lane-scratch offset, count, offset inside the chunk's segment (written by
+    // one lane, read by others after __syncwarp: accessed with ld/st.cg, L2 only)
+    uint32_t u_soff[MAXU], u_cnt[MAXU], u_pre[MAXU];
+    unsigned long long c_t[MAXC];          // claim time (gls_config.trace; lane 0 only)
+    unsigned long long lcyc[32];           // per-lane clocks spent in unit set-up (own lane only)
+    uint32_t lit[32], lsu[32];             // per-lane iterations / unit set-ups of the batch (trace)
 };
 __device__ __forceinline__ WarpAux& warp_aux(const SimParams& p) {
     return reinterpret_cast<WarpAux*>(p.waux)[warp_global_id()];
+}
+// the same, recomputed at each use (an opaque base: not hoisted out of the sweep loop, where
+// a live 64-bit address would cost registers the entry path needs)
+__device__ __forceinline__ WarpAux& warp_aux_cold(const SimParams& p) {
+    void* a;
+    asm volatile("mov.b64 %0, %1;" : "=l"(a) : "l"(p.waux));
+    return reinterpret_cast<WarpAux*>(a)[warp_global_id()];
 }
 
 // Shared memory of a CTA (namespace scope, so addresses are constants plus the thread
 // index, not registers): the 4-value LUT (a3, staged per CTA), then per-thread delay
 // tables (u16 [24][kThreads]), one Batch per warp, the per-thread pin cursor columns.
-constexpr int kDtabWords = 24;
+constexpr int kDtabWords = 16;                   // u16 halves of 8 words [pin][edge] = d(->0) | d(->1) << 16
 __shared__ uint8_t g_lut[kLutCap];
 extern __shared__ __align__(16) unsigned char g_dyn[];
 constexpr size_t kDynBytes = (size_t)kDtabWords * kThreads * 2 + kBatchBytes * (kThreads / 32) + kPinSmBytes;
@@ -225,7 +233,7 @@ __device__ __forceinline__ PinSm pin_cols() {
     return PinSm{(uint32_t)__cvta_generic_to_shared(g_dyn + (size_t)kDtabWords * kThreads * 2 +
                                                     kBatchBytes * (kThreads / 32))};
 }
-__device__ __forceinline__ uint16_t* dtab_cols() { return reinterpret_cast<uint16_t*>(g_dyn); }
+__device__ __forceinline__ uint32_t* dtab_cols() { return reinterpret_cast<uint32_t*>(g_dyn); }
 __device__ __forceinline__ uint32_t lut_sa() { return (uint32_t)__cvta_generic_to_shared(g_lut); }
 
 __device__ __forceinline__ void acc_zero(Batch& B) {
@@ -249,13 +257,11 @@ __device__ __forceinline__ void fill_dtab(T* dtab, int dstride, const ChunkSetup
         const uint4 d = s.d[i];
         // (GLS_DELAY_INF -> 0xFFFF, above every finite delay of a gate on this path; the min
         // for X then takes the related one)
+        // (word [pin][edge]: edge 0 = FALL (z, w), 1 = RISE (x, y); the X delay is the min of
+        // the halves, taken in the sweep)
         const uint32_t z = min(d.z, 0xFFFFu), w = min(d.w, 0xFFFFu), x = min(d.x, 0xFFFFu), y = min(d.y, 0xFFFFu);
-        dtab[(i * 6 + 0) * dstride] = (T)z;
-        dtab[(i * 6 + 1) * dstride] = (T)w;
-        dtab[(i * 6 + 2) * dstride] = (T)min(z, w);
-        dtab[(i * 6 + 3) * dstride] = (T)x;
-        dtab[(i * 6 + 4) * dstride] = (T)y;
-        dtab[(i * 6 + 5) * dstride] = (T)min(x, y);
+        dtab[(i * 2 + 0) * dstride] = (T)(z | w << 16);
+        dtab[(i * 2 + 1) * dstride] = (T)(x | y << 16);
     }
 }
 
@@ -287,7 +293,7 @@ __device__ __noinline__ void fallback_count(const SimParams& p, Batch& B, int u,
             run_chunk<false, true>(p, s, lut, nullptr, p.deep + at, dcap, r);
         }
     }
-    B.u_cnt[u] = r.cnt;
+    __stcg(&X.u_cnt[u], r.cnt);
     B.u_vb[u] = (uint8_t)r.vb;
     evals += r.evals;
     events += r.events;
@@ -305,7 +311,7 @@ __device__ __noinline__ void fallback_write(const SimParams& p, const Batch& B, 
         run_chunk<true, true>(p, s, lut, dst,
                               p.deep + (unsigned long long)warp_global_id() * p.deep_per_warp + dofs, dcap, r);
     }
-    if (r.cnt != B.u_cnt[u] || r.overflow) atomicOr(&p.ctl->error, kErrBug);
+    if (r.cnt != __ldcg(&warp_aux(p).u_cnt[u]) || r.overflow) atomicOr(&p.ctl->error, kErrBug);
 }
 
 // per-base thresholds (entry form, relative to B = b4 >> 2): t >= T0 <=> e >= t0q;
@@ -532,18 +538,19 @@ __device__ __forceinline__ void unit_end(const SimParams& p, Batch& B, int u, ui
         // the fallback counts the whole unit again: take back what this partial run counted
         const int lane = threadIdx.x & 31;
         B.u_st[u] = 1;
-        B.lev[lane] -= B.lev[lane] + (l_cnt & 0xffffu) - warp_aux(p).u_sev[u];
-        B.levt[lane] -= B.levt[lane] + (l_cnt >> 16) - warp_aux(p).u_sevt[u];
+        B.lev[lane] -= B.lev[lane] + (l_cnt & 0xffffu) - warp_aux_cold(p).u_sev[u];
+        B.levt[lane] -= B.levt[lane] + (l_cnt >> 16) - warp_aux_cold(p).u_sevt[u];
         return;
     }
     const uint64_t* scr = p.wscr + sbase;
     const long long T0 = B.u_T0[u], T1e = min(B.u_T1[u], p.duration + 1);
-    uint32_t lo = used, hi = n;                                          // (times: arithmetic shift of the entry)
+    uint32_t lo = used, hi = n, vb = 2u;
     while (lo < hi && ((long long)scr[lo] >> 2) < T0) ++lo;
     while (hi > lo && ((long long)scr[hi - 1] >> 2) >= T1e) --hi;
-    B.u_soff[u] = lo;
-    B.u_cnt[u] = hi - lo;
-    B.u_vb[u] = (uint8_t)(lo > used ? (uint32_t)(scr[lo - 1] & 3u) : 2u);
+    if (lo > used) vb = (uint32_t)(scr[lo - 1] & 3u);
+    __stcg(&warp_aux_cold(p).u_soff[u], lo);
+    __stcg(&warp_aux_cold(p).u_cnt[u], hi - lo);
+    B.u_vb[u] = (uint8_t)vb;
     used = hi;
 }
 
@@ -580,8 +587,8 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
     B.pend[lane] = -1;
     B.lane_first[lane] = B.lane_last[lane] = -1;
     B.lev[lane] = B.levt[lane] = 0;
-    B.lcyc[lane] = 0;
-    B.lit[lane] = B.lsu[lane] = 0;
+    warp_aux_cold(p).lcyc[lane] = 0;
+    warp_aux_cold(p).lit[lane] = warp_aux_cold(p).lsu[lane] = 0;
     __syncwarp();
 
     for (;;) {
@@ -609,7 +616,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 // nothing but constants lives across the set-up call: the round's counts, the
                 // iteration and the scratch fill go through shared memory (set-up path only)
                 B.lev[lane] += l_cnt & 0xffffu;
-            B.lit[lane] += (uint32_t)it;
+            warp_aux_cold(p).lit[lane] += (uint32_t)it;
                 B.levt[lane] += l_cnt >> 16;
                 l_cnt = 0;
                 B.sv_it[lane] = (uint8_t)it;
@@ -619,10 +626,10 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 const bool fast = unit_begin(p, u, ui);
                 {
                     const unsigned long long dc = (unsigned long long)(clock64() - c_u0);
-                    B.lcyc[lane] += dc;
+                    warp_aux_cold(p).lcyc[lane] += dc;
                     if (lane == __ffs(__activemask()) - 1) B.acc[A_BAL + 4] += dc;   // warp-level: one pass
                 }
-                B.lsu[lane] += 1;
+                warp_aux_cold(p).lsu[lane] += 1;
                 it = B.sv_it[lane];
                 used = B.sv_used[lane];
                 if (!fast) {                                             // long delays: per-lane ring engine
@@ -640,9 +647,9 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 t0q = ui.t0q;
                 lim = ui.lim;
                 asm volatile("" ::: "memory");                           // (keeps the copies in registers: ui is dead)
-                warp_aux(p).u_sev[u] = B.lev[lane];                      // counts so far (a fallback takes them back)
+                warp_aux_cold(p).u_sev[u] = B.lev[lane];                      // counts so far (a fallback takes them back)
                 B.u_r0[u] = (uint16_t)B.round;
-                warp_aux(p).u_sevt[u] = B.levt[lane];
+                warp_aux_cold(p).u_sevt[u] = B.levt[lane];
                 n = used;
                 nfl = used | (2u << 16);                                 // nothing final yet; value before: X
                 top = 0;
@@ -721,7 +728,9 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                         // rise iff rank(new) > rank(old), rank 0 < X < 1 on normalised codes (R2):
                         // (old, new) in {(0,1), (0,X), (X,1)} = bits 1, 2, 9 of (old << 2 | new)
                         const uint32_t rise = (0x206u >> ((((xn >> b) & 3u) << 2) | ((nn >> b) & 3u))) & 1u;
-                        del = min(del, lds16(dt_sa + (uint32_t)((b >> 1) * 6 + (int)rise * 3 + (int)E) * (kThreads * 2)));  // min rule
+                        const uint32_t dw = lds32(dt_sa + (uint32_t)((b >> 1) * 2 + (int)rise) * (kThreads * 4));
+                        // (E = 0, 1: the half; X: the smaller half, R1) — min rule
+                        del = min(del, E == 2u ? min(dw & 0xFFFFu, dw >> 16) : __funnelshift_r(dw, 0u, 16u * E) & 0xFFFFu);
                         cm &= cm - 1;
                     } while (cm);
                     const uint32_t rq = ((tq >> 2) + del) << 2;         // appearance time, entry form
@@ -755,7 +764,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         {
             const unsigned itmax = __reduce_max_sync(FULL, (unsigned)it), itsum = __reduce_add_sync(FULL, (unsigned)it);
             B.lev[lane] += l_cnt & 0xffffu;
-            B.lit[lane] += (uint32_t)it;
+            warp_aux_cold(p).lit[lane] += (uint32_t)it;
             B.levt[lane] += l_cnt >> 16;
             l_cnt = 0;
             if (lane == 0) {
@@ -826,7 +835,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         __syncwarp();
     }
     const unsigned ev = __reduce_add_sync(FULL, B.lev[lane]), evt = __reduce_add_sync(FULL, B.levt[lane]);
-    const unsigned long long sc = warp_sum64(B.lcyc[lane]);
+    const unsigned long long sc = warp_sum64(warp_aux_cold(p).lcyc[lane]);
     if (lane == 0) {
         B.acc[A_EVALS] += ev;
         B.acc[A_EVENTS] += evt;
@@ -938,7 +947,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             units_needed += need;
             B.c_inf[nc] = (p.gate[g].flags & kGateInf) != 0;
             B.id[nc] = id;
-            B.c_t[nc] = p.trace ? gtimer() : 0ull;
+            warp_aux(p).c_t[nc] = p.trace ? gtimer() : 0ull;
             est[nc] = e;
             total += e;
             ++nc;
@@ -1049,8 +1058,8 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
     for (int j = lane; j < nc; j += 32) {
         uint32_t tot = 0;
         for (int v = B.c_first[j]; v != kEnd; v = B.u_next[v]) {
-            B.u_pre[v] = tot;
-            tot += B.u_cnt[v];
+            __stcg(&warp_aux(p).u_pre[v], tot);
+            tot += __ldcg(&warp_aux(p).u_cnt[v]);
         }
         unsigned long long off = tot ? atomicAdd(&p.ctl->arena_top, seg_round(tot)) : 0ull;
         if (off + tot > p.arena_cap) {
@@ -1065,14 +1074,14 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
     // ---- each lane moves its units into place (independent loads, overlapped latency)
     for (int v = B.lane_first[lane]; v >= 0; v = B.u_lnext[v]) {
         const unsigned long long off = B.c_off[B.u_chunk[v]];
-        const uint32_t cu = B.u_cnt[v];
+        const uint32_t cu = __ldcg(&warp_aux(p).u_cnt[v]);
         if (off == ~0ull || cu == 0) continue;
-        uint64_t* dst = p.arena + off + B.u_pre[v];
+        uint64_t* dst = p.arena + off + __ldcg(&warp_aux(p).u_pre[v]);
         if (B.u_st[v] != 0) {
             fallback_write(p, B, v, lut, dst);
             continue;
         }
-        const uint64_t* src = p.wscr + (warp_global_id() * 32u + (uint32_t)lane) * (uint32_t)LCAP + B.u_soff[v];
+        const uint64_t* src = p.wscr + (warp_global_id() * 32u + (uint32_t)lane) * (uint32_t)LCAP + __ldcg(&warp_aux(p).u_soff[v]);
         uint32_t e = 0;
         for (; e + 4 <= cu; e += 4) {
             const uint64_t a0 = src[e], a1 = src[e + 1], a2 = src[e + 2], a3 = src[e + 3];
@@ -1087,8 +1096,8 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
     const long long c_out = clock64();
     unsigned long long t_maxit = 0, t_maxsu = 0;
     if (p.trace) {
-        t_maxit = __reduce_max_sync(FULL, B.lit[lane]);
-        t_maxsu = __reduce_max_sync(FULL, B.lsu[lane]);
+        t_maxit = __reduce_max_sync(FULL, warp_aux(p).lit[lane]);
+        t_maxsu = __reduce_max_sync(FULL, warp_aux(p).lsu[lane]);
     }
     // ---- complete the chunks (whole warp, one after the other)
     for (int j = 0; j < nc; ++j) {
@@ -1104,7 +1113,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         R.evals = 0;                                   // (counted per lane above)
         R.events = 0;
         if (p.trace && lane == 0) {
-            const unsigned long long d = gtimer() - B.c_t[j];
+            const unsigned long long d = gtimer() - warp_aux(p).c_t[j];
             unsigned long long* tr = p.trace + 8ull * R.gi;
             atomicAdd(&tr[2], d);
             if (atomicMax(&tr[3], d) < d) {                 // the slowest chunk's batch (racy only across chunks)
