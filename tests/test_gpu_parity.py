@@ -27,8 +27,11 @@ def run_oracle(nl, st, dur):
 
 # engine 0 = lanes on re-balanced time-slice units (default), 1 = one chunk per lane;
 # scheduler 0 = dataflow (default), 1 = level barriers
-ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1)]
-EIDS = ["units-df", "units-lvl", "lane"]
+ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1), dict(engine=3)]
+EIDS = ["units-df", "units-lvl", "lane", "auto"]
+# the engines running the 32-bit sweep (rebase, u16 delay table, long-delay fallback)
+SWEEP = [ENGINES[0], ENGINES[1], ENGINES[3]]
+SIDS = [EIDS[0], EIDS[1], EIDS[3]]
 # engine 2 = the paper's CSRP pages + Alg. 1 (A/B baseline), small page lengths included
 CSRP = [dict(engine=2), dict(engine=2, csrp_pagelen=2), dict(engine=2, csrp_pagelen=7)]
 CIDS = ["csrp256", "csrp2", "csrp7"]
@@ -132,7 +135,7 @@ def test_large_times(ctx, engine):
     assert_same(ctx, nl, W.stimuli_from_lists(waves), 13 * (1 << 29), **engine)
 
 
-@pytest.mark.parametrize("engine", ENGINES[:2], ids=EIDS[:2])
+@pytest.mark.parametrize("engine", SWEEP, ids=SIDS)
 @pytest.mark.parametrize("lo,hi", [(5000, 5200), (0, 1000), (60000, 70000)])
 def test_delay_spread_paths(ctx, lo, hi, engine):
     """Delays below 2^16 take the 32-bit sweep (u16 delay table), larger ones the per-lane
@@ -143,7 +146,7 @@ def test_delay_spread_paths(ctx, lo, hi, engine):
         assert_same(ctx, nl, st, 40 * hi + 500, chunk_events=int(7 + 5 * seed), **engine)
 
 
-@pytest.mark.parametrize("engine", ENGINES[:2], ids=EIDS[:2])
+@pytest.mark.parametrize("engine", SWEEP, ids=SIDS)
 @pytest.mark.parametrize("seed", range(4))
 def test_rebase_boundaries(ctx, seed, engine):
     """Glitch-dense bursts straddling multiples of 2^29 ps: the 32-bit sweep moves its

@@ -1,0 +1,9 @@
+set -u
+T=r02h; O=gpurun_out/$T; mkdir -p $O
+
+
+for e in 3 0; do
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:sim_kernel -s 1 -c 1 -o $O/e${e}_c3 \
+  python bench.py --engine $e --config c3_1m --steps 1 --warmup 1 --no-cpu-baseline --no-e2e > $O/ncu_e$e.log 2>&1
+tail -1 $O/ncu_e$e.log
+done
