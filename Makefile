@@ -4,7 +4,7 @@ ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall --expt-relaxed-constexpr
 PKG := paper_2304_13398_b200
 SRC := $(PKG)/csrc/gls_api.cu $(PKG)/csrc/gls_kernels.cu
-HDR := $(PKG)/csrc/gls_internal.cuh $(PKG)/csrc/gls_lanes.cuh $(PKG)/csrc/gls_auto.cuh $(PKG)/csrc/gls_csrp.cuh include/gls.h
+HDR := $(PKG)/csrc/gls_internal.cuh $(PKG)/csrc/gls_lanes.cuh $(PKG)/csrc/gls_csrp.cuh include/gls.h
 
 all: $(PKG)/libgls.so oracle/liboracle.so
 

@@ -217,7 +217,7 @@ int64_t free_bytes(gls_ctx* ctx) {
     return (int64_t)fr;
 }
 
-int default_M(int engine) { return engine == 0 ? 16384 : engine == 3 ? 2048 : 256; }
+int default_M(int engine) { return engine == 0 ? 16384 : 256; }
 
 SimParams params(gls_ctx* ctx) {
     SimParams p{};
@@ -421,8 +421,7 @@ void gls_destroy(gls_ctx* ctx) {
 int gls_set_config(gls_ctx* ctx, const gls_config* cfg) {
     if (!ctx || !cfg) return GLS_EINVAL;
     if (cfg->arena_bytes < 0 || cfg->chunk_capacity < 0 || cfg->chunk_events < 0 || cfg->blocks_per_sm < 0 ||
-        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 3 ||
-        (cfg->engine == 3 && cfg->scheduler != 0) ||
+        cfg->ring_limit < 0 || cfg->ring_limit > kRing || cfg->engine < 0 || cfg->engine > 2 ||
         cfg->scheduler < 0 || cfg->scheduler > 1 || cfg->deep_per_warp < 0 || cfg->readback_mib < 0 ||
         cfg->trace < 0 || cfg->trace > 1 || cfg->csrp_pagelen == 1 || cfg->csrp_pagelen < 0)
         return fail(ctx, GLS_EINVAL, "invalid gls_config field");
@@ -896,11 +895,9 @@ static int simulate_run(gls_ctx* ctx, int64_t duration) {
     int sms = per_sm ? maxb / per_sm : 0;
     int blocks = ctx->cfg.blocks_per_sm > 0 ? std::min(maxb, ctx->cfg.blocks_per_sm * sms) : maxb;
     if (blocks < 1) return fail(ctx, GLS_ECUDA, "simulation kernel cannot be resident (occupancy 0)");
-    if (ctx->cfg.engine == 0) {     // engine 0's lane scratch / per-warp unit fields (engine 3 writes in place)
+    if (ctx->cfg.engine == 0) {     // engine 0's lane scratch and per-warp unit fields
         if (ctx->d_wscr.n < warp_scratch_entries(blocks)) CK(ctx->d_wscr.alloc(warp_scratch_entries(blocks)));
         if (ctx->d_waux.n < warp_aux_bytes(blocks)) CK(ctx->d_waux.alloc(warp_aux_bytes(blocks)));
-    } else if (ctx->cfg.engine == 3) {   // engine 3: one chunk record per lane
-        if (ctx->d_waux.n < auto_lane_bytes(blocks)) CK(ctx->d_waux.alloc(auto_lane_bytes(blocks)));
     }
     const int64_t nwarps = (int64_t)blocks * (kThreads / 32);
     if (ctx->deep_per_warp == 0) ctx->deep_per_warp = ctx->cfg.deep_per_warp > 0 ? ctx->cfg.deep_per_warp : (1 << 16);

@@ -125,7 +125,6 @@ cudaError_t launch_init_given(const SimParams& p, const long long* in_off, cudaS
 cudaError_t launch_simulate(const SimParams& p, int blocks, cudaStream_t s);
 size_t warp_scratch_entries(int blocks);
 size_t warp_aux_bytes(int blocks);
-size_t auto_lane_bytes(int blocks);        // engine 3: per-lane chunk records
 // engine 2 (CSRP pages + Alg. 1, gls_csrp.cuh)
 int csrp_coresident_threads(int device);
 size_t csrp_scratch_entries(int threads);

@@ -789,7 +789,6 @@ __device__ void chunk_done(const SimParams& p, unsigned long long id, const Chun
 
 }  // namespace gls
 #include "gls_lanes.cuh"
-#include "gls_auto.cuh"
 namespace gls {
 constexpr int kCsrpStack = 1024;    // engine 2: a thread's individual memory (entries)
 }
@@ -799,11 +798,8 @@ namespace gls {
 #ifndef GLS_MINB
 #define GLS_MINB 3
 #endif
-#ifndef GLS_MINB3
-#define GLS_MINB3 2     // engine 3: 2 CTAs per SM (its shared memory), 128 registers
-#endif
 template <int ENGINE, bool DATAFLOW>
-__global__ void __launch_bounds__(kThreads, ENGINE == 3 ? GLS_MINB3 : GLS_MINB) sim_kernel(const __grid_constant__ SimParams p) {
+__global__ void __launch_bounds__(kThreads, GLS_MINB) sim_kernel(const __grid_constant__ SimParams p) {
     uint8_t* const s_lut = ln::g_lut;
     for (int i = threadIdx.x; i < kLutCap; i += blockDim.x) s_lut[i] = p.lut[i];
     __syncthreads();
@@ -811,11 +807,6 @@ __global__ void __launch_bounds__(kThreads, ENGINE == 3 ? GLS_MINB3 : GLS_MINB) 
     const unsigned warps_per_block = blockDim.x >> 5;
     const unsigned gwarp = blockIdx.x * warps_per_block + (threadIdx.x >> 5);
     const unsigned nwarps = gridDim.x * warps_per_block;
-    if (ENGINE == 3) {                                  // autonomous lanes (dataflow only)
-        for (int g = (int)gwarp; g < p.level_off[1]; g += (int)nwarps) plan_gate(p, (uint32_t)g);
-        au::run(p);
-        return;
-    }
     if (DATAFLOW) {
         // seed: gates fed only by given nets (topological level 1) are ready now
         for (int g = (int)gwarp; g < p.level_off[1]; g += (int)nwarps) plan_gate(p, (uint32_t)g);
@@ -1124,11 +1115,10 @@ __global__ void fanin_reads_kernel(const unsigned long long* len, const uint32_t
 
 // ------------------------------------------------------------------ launchers
 static size_t dyn_smem(int engine) {
-    return engine == 0 ? ln::kDynBytes : engine == 3 ? au::kDynBytes : 0;
+    return engine == 0 ? ln::kDynBytes : 0;
 }
 static const void* kernel_for(int engine, int sched) {
     if (engine == 1) return (const void*)sim_kernel<1, false>;
-    if (engine == 3) return (const void*)sim_kernel<3, true>;
     return sched == 1 ? (const void*)sim_kernel<0, false> : (const void*)sim_kernel<0, true>;
 }
 
@@ -1144,7 +1134,7 @@ int max_coresident_blocks(int device, int engine, int sched, int* per_sm) {
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_smem(engine));
     // shared-memory carveout: just what the resident CTAs need (the rest stays L1, which
     // caches the fan-in entries the sweep reads: engine 0 at 3 CTAs/SM keeps ~92 KB)
-    if (engine == 0 || engine == 3) {
+    if (engine == 0) {
         cudaFuncAttributes fa{};
         cudaFuncGetAttributes(&fa, k);
         int maxsm = 0, want = 3;

@@ -56,7 +56,7 @@ constexpr int W_LANE = GLS_WLANE;                // a batch is filled up to 32 x
 #endif
 constexpr int W_MIN = GLS_WMIN;                  // fewest expected entries per static unit
 #ifndef GLS_ROUND
-#define GLS_ROUND 32
+#define GLS_ROUND 512
 #endif
 constexpr int ROUND = GLS_ROUND;                 // sweep iterations between re-balancing points
 #ifndef GLS_MQ_MIN
@@ -190,7 +190,7 @@ struct Batch {
     int nun;                               // units (static + split)
     int8_t pend[32];                       // unit handed to a lane by a split (-1: none)
     uint32_t lev[32], levt[32];            // per-lane gate-evals / events of the batch
-    uint8_t sv_it[32];                     // (set-up call: the lane's round iteration,
+    uint16_t sv_it[32];                    // (set-up call: the lane's round iteration,
     uint16_t sv_used[32];                  //  scratch fill)
     int8_t u_lnext[MAXU];                  // next unit taken by the same lane (-1: last)
     int8_t lane_first[32], lane_last[32];  // the lane's units in the order it took them
@@ -619,7 +619,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
             warp_aux_cold(p).lit[lane] += (uint32_t)it;
                 B.levt[lane] += l_cnt >> 16;
                 l_cnt = 0;
-                B.sv_it[lane] = (uint8_t)it;
+                B.sv_it[lane] = (uint16_t)it;
                 B.sv_used[lane] = (uint16_t)used;
                 UnitInit ui;                                             // (local memory: set-up path only)
                 const long long c_u0 = clock64();

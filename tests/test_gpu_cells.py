@@ -12,8 +12,8 @@ from paper_2304_13398_b200 import gls
 from paper_2304_13398_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
-ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1), dict(engine=3)]
-EIDS = ["units-df", "units-lvl", "lane", "auto"]
+ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1)]
+EIDS = ["units-df", "units-lvl", "lane"]
 
 
 @pytest.fixture(scope="module")

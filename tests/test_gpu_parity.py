@@ -27,11 +27,11 @@ def run_oracle(nl, st, dur):
 
 # engine 0 = lanes on re-balanced time-slice units (default), 1 = one chunk per lane;
 # scheduler 0 = dataflow (default), 1 = level barriers
-ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1), dict(engine=3)]
-EIDS = ["units-df", "units-lvl", "lane", "auto"]
+ENGINES = [dict(engine=0), dict(engine=0, scheduler=1), dict(engine=1)]
+EIDS = ["units-df", "units-lvl", "lane"]
 # the engines running the 32-bit sweep (rebase, u16 delay table, long-delay fallback)
-SWEEP = [ENGINES[0], ENGINES[1], ENGINES[3]]
-SIDS = [EIDS[0], EIDS[1], EIDS[3]]
+SWEEP = ENGINES[:2]
+SIDS = EIDS[:2]
 # engine 2 = the paper's CSRP pages + Alg. 1 (A/B baseline), small page lengths included
 CSRP = [dict(engine=2), dict(engine=2, csrp_pagelen=2), dict(engine=2, csrp_pagelen=7)]
 CIDS = ["csrp256", "csrp2", "csrp7"]
