@@ -164,6 +164,26 @@ def oracle_sample(nl, spec, cycles):
     return r, dt, dur
 
 
+def _oracle_set_worker(args):
+    """(spawned process) the oracle as it stands on one stimulus set's first `cycles` cycles"""
+    cfg, seed, cycles = args
+    nl = W.config_netlist(cfg, 1)
+    spec = W.config_stimspec(cfg, seed)
+    r, dt, _ = oracle_sample(nl, spec, cycles)
+    return r.gate_evals, dt
+
+
+def oracle_sets_concurrent(cfg, seeds, cycles):
+    """C5's CPU baseline: min(64, nproc) single-thread oracle processes, one per
+    stimulus set, run concurrently; aggregate gate-evals / the slowest process's time."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    with cf.ProcessPoolExecutor(max_workers=len(seeds), mp_context=mp.get_context("spawn")) as ex:
+        res = list(ex.map(_oracle_set_worker, [(cfg, s, cycles) for s in seeds]))
+    evals = sum(r[0] for r in res)
+    return evals, max(r[1] for r in res)
+
+
 def run_reference(a):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -435,6 +455,49 @@ def run_gls(a):
                       (f", first {len(e_sets)} of the rank's {len(stims)} stimulus sets" if len(stims) > 1 else "")}
         del pinned
 
+    # e2e with a WAVEFORM readback (a10): each step H2D of the given waveforms (pinned), simulate,
+    # then the canonical CSR of every net restricted to the first 1/32 of the duration
+    # gathered on the device (gls_get_waveforms_range_device) and read back into pinned host
+    # memory — the transitions themselves, not their checksums
+    e2e_w = None
+    if not a.no_e2e and len(stims) == 1 and world == 1:
+        try:
+            o_, t_, n_ = stims[0]
+            h_off = torch.empty(o_.numel(), dtype=torch.int64, pin_memory=True)
+            h_tr = torch.empty(n_, dtype=torch.int64, pin_memory=True)
+            h_off.copy_(o_)
+            h_tr.copy_(t_)
+            t_hi = duration // 32
+            nn = nl.num_nets
+            d_o = torch.empty(nn + 1, dtype=torch.int64, device=dev)
+            tot = ctx.gls_get_waveforms_range_device(0, nn, 0, t_hi, d_o.data_ptr())
+            d_w = torch.empty(max(1, int(tot * 1.05) + 1024), dtype=torch.int64, device=dev)
+            h_w = torch.empty(d_w.numel(), dtype=torch.int64, pin_memory=True)
+            h_o = torch.empty(nn + 1, dtype=torch.int64, pin_memory=True)
+            n_e = max(1, min(a.steps, 2))
+            torch.cuda.synchronize(dev)
+            w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            w0.record(stream)
+            d2h = 0
+            for _ in range(n_e):
+                ctx.gls_set_input_waveforms(nl.num_inputs, h_off.numpy(), h_tr.numpy().view(np.uint64))
+                ctx.gls_simulate(duration)
+                tot = ctx.gls_get_waveforms_range_device(0, nn, 0, t_hi, d_o.data_ptr(), d_w.data_ptr(), d_w.numel())
+                h_o.copy_(d_o, non_blocking=True)
+                h_w[:tot].copy_(d_w[:tot], non_blocking=True)
+                d2h = 8 * (nn + 1 + tot)
+            w1.record(stream)
+            torch.cuda.synchronize(dev)
+            w_ms = w0.elapsed_time(w1) / n_e
+            e2e_w = {"value": units / (w_ms / 1e3), "unit": "gate-evals/s", "ms_per_step": w_ms,
+                     "h2d_bytes_per_step": int(8 * (o_.numel() + n_)), "d2h_bytes_per_step": int(d2h),
+                     "window_ps": [0, int(t_hi)], "transitions_read_back": int(tot),
+                     "api": "gls_set_input_waveforms(host pinned) + gls_simulate + gls_get_waveforms_range_device "
+                            "(all nets, first 1/32 of the duration) + D2H into pinned host memory"}
+            del d_o, d_w, h_w, h_o, h_off, h_tr
+        except Exception as e:                  # (a device buffer that does not fit beside the arena)
+            e2e_w = {"error": repr(e)[:200]}
+
     # a10 at full size: the canonical CSR of the whole result through the public host API
     # (device gather in net order, batch by batch through a staging buffer, one D2H each),
     # timed once on rank 0 when it fits comfortably in host memory
@@ -473,12 +536,24 @@ def run_gls(a):
         parity = {"window_ps": [0, tmax], "nets": int(gh.size), "hash_mismatches": mism,
                   "bit_exact": mism == 0}
         log(f"oracle sample: {r.gate_evals} gate-evals in {dt:.2f}s; parity mismatches {mism}")
+        if replicas:
+            # independent stimulus sets: one single-thread oracle process per set, concurrently
+            k = max(1, min(C5_SETS, os.cpu_count() or 1))
+            try:
+                ev, wall = oracle_sets_concurrent(cfg, [a.seed + j for j in range(k)], cyc)
+                cpu.update({"value": ev / wall, "cores": k,
+                            "sample": f"{cfg}: {k} stimulus sets (seeds {a.seed}..{a.seed + k - 1}) in {k} concurrent "
+                                      f"single-thread oracle processes, first {cyc} of {nc} clock cycles each: "
+                                      f"{ev} gate-evals, slowest process {wall:.2f} s",
+                            "single_process_value": r.gate_evals / dt})
+            except Exception as e:
+                log(f"concurrent oracle failed: {e!r}")
 
     if rank == 0:
         peak, peak_src = load_peaks()
         achieved = alg / (kms / 1e3) / 1e9
         traffic = None
-        tp = os.path.join(ROOT, "profiles", "traffic_r01.json")
+        tp = os.path.join(ROOT, "profiles", "traffic_r02.json")
         if os.path.exists(tp):
             try:
                 with open(tp) as f:
@@ -503,7 +578,8 @@ def run_gls(a):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "gls::sim_kernel", "kernel_ms": kms, "alg_bytes_per_launch": alg},
-            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "stitch": stitch, "readback": readback,
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e, "e2e_waveforms": e2e_w, "stitch": stitch,
+            "readback": readback,
             # per step: init_given_kernel + sim_kernel (gls_simulate) and fanin_reads_kernel
             # (gls_get_stats' algorithmic-bytes count, read after every step for kernel_ms)
             # (C5: + validate_kernel of gls_set_input_waveforms_device per set)

@@ -31,7 +31,7 @@ ncyc = int(sys.argv[1]) if len(sys.argv) > 1 else 60000
 ctx = gls.Context(0, torch.cuda.current_stream(dev).cuda_stream)
 ctx.load(nl)
 mean = max(50, c["mean_trans"] * ncyc // c["ncycles"])   # the same mean activity in every run
-for target in [None, 1.0, 4.0, 17.0, 50.0]:
+for target in [None, 1.0, 4.0, 17.1, 54.5]:   # 17.1, 54.5: NVDLA_c, NVDLA_o
     # "random": every PI toggles with p = 0.5 per cycle, so 2 * mean cycles give the same mean
     spec = (W.make_stimspec(1, c["num_inputs"], 2 * mean, "random") if target is None else
             W.make_stimspec(1, c["num_inputs"], ncyc, "skewed", mean, target))
