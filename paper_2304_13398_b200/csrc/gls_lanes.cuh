@@ -62,9 +62,6 @@ constexpr int ROUND = GLS_ROUND;                 // sweep iterations between re-
 #ifndef GLS_MQ_MIN
 #define GLS_MQ_MIN 0                             // chunks with at least this many expected entries are
 #endif                                           // sliced at merged-count quantiles (0: never)
-#ifndef GLS_COLREG
-#define GLS_COLREG 0                             // cursor-column bases in opaque registers (A/B)
-#endif
 #ifndef GLS_MINSPLIT
 #define GLS_MINSPLIT 64
 #endif
@@ -575,13 +572,6 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
     const uint32_t sbase = (warp_global_id() * 32u + (uint32_t)lane) * (uint32_t)LCAP;
     uint64_t* const scr = p.wscr + sbase;
     const uint32_t dt_sa = (uint32_t)__cvta_generic_to_shared(dtab_cols() + tid);   // [q * blockDim.x + tid]
-#if GLS_COLREG
-    // this thread's cursor-column bases (8-byte columns: ptr, hn; 4-byte: rem, ck) held in
-    // opaque registers, so the per-entry addresses are one IMAD from the pin index
-    uint32_t pb, rb;
-    asm volatile("mov.u32 %0, %1;" : "=r"(pb) : "r"(cs.ptr(tid)));
-    asm volatile("mov.u32 %0, %1;" : "=r"(rb) : "r"(cs.rem(tid)));
-#endif
     int u = -1;                            // current unit
     uint32_t used = 0;                     // lane scratch fill
     uint32_t l_cnt = 0;                    // this round's gate-evals (bits 0-15) and events (16-31), <= ROUND each
@@ -695,33 +685,27 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 // ---- one fan-in entry: the pin with the smallest head
                 const int b = h0 == m ? 0 : h1 == m ? 1 : h2 == m ? 2 : 3;
                 nr = (nr & ~(3u << (2 * b))) | ((m & 3u) << (2 * b));
-#if GLS_COLREG
-                const uint32_t a8 = pb + (uint32_t)b * (kThreads * 8u), a4 = rb + (uint32_t)b * (kThreads * 4u);
-                const uint32_t a_ptr = a8, a_hn = a8 + 4u * kThreads * 16u, a_rem = a4, a_ck = a4 + 4u * kThreads * 4u;
-#else
                 const int ci = b * kThreads + tid;
-                const uint32_t a_ptr = cs.ptr(ci), a_hn = cs.hn(ci), a_rem = cs.rem(ci), a_ck = cs.ck(ci);
-#endif
-                const uint64_t* ptr = (const uint64_t*)lds64(a_ptr) + 1;
-                uint32_t rem = lds32(a_rem) - 1u;
+                const uint64_t* ptr = (const uint64_t*)lds64(cs.ptr(ci)) + 1;
+                uint32_t rem = lds32(cs.rem(ci)) - 1u;
                 cp_wait_pin(b, lastpin);                                 // the pin's lookahead has landed
-                uint64_t hn = lds64(a_hn);
+                uint64_t hn = lds64(cs.hn(ci));
                 if (rem == 0) {                                          // segment end: next non-empty segment
-                    const Seg g = next_segment(p, lds32(a_ck), unit_src(p, B, u, b));
+                    const Seg g = next_segment(p, lds32(cs.ck(ci)), unit_src(p, B, u, b));
                     if (g.rem) {
                         ptr = g.ptr;
                         rem = g.rem;
-                        sts32(a_ck, g.ck);
+                        sts32(cs.ck(ci), g.ck);
                         hn = ldg_entry(ptr);
                     } else {
                         hn = kInfEntry;
                     }
                 }
                 const uint32_t nh = rem ? to_rel(hn, b4) : kRelInf;
-                cp_async8_if(rem > 1, a_hn, ptr + 1);                    // nothing waits for it until pin b moves again
+                cp_async8_if(rem > 1, cs.hn(ci), ptr + 1);               // nothing waits for it until pin b moves again
                 lastpin = rem > 1 ? b : lastpin;
-                sts64(a_ptr, (uint64_t)ptr);
-                sts32(a_rem, rem);
+                sts64(cs.ptr(ci), (uint64_t)ptr);
+                sts32(cs.rem(ci), rem);
                 h0 = b == 0 ? nh : h0;
                 h1 = b == 1 ? nh : h1;
                 h2 = b == 2 ? nh : h2;

@@ -27,7 +27,8 @@ def run(ctx, spec, dev, sched, steps=2, warm=2):
 dev = torch.device("cuda", 0)
 nl = W.config_netlist("c4_mini", 1)
 c = W.CONFIGS["c4_mini"]
-ncyc = int(sys.argv[1]) if len(sys.argv) > 1 else 60000
+c4_cycles = c["ncycles"]
+ncyc = int(sys.argv[1]) if len(sys.argv) > 1 else c4_cycles
 ctx = gls.Context(0, torch.cuda.current_stream(dev).cuda_stream)
 ctx.load(nl)
 mean = max(50, c["mean_trans"] * ncyc // c["ncycles"])   # the same mean activity in every run
