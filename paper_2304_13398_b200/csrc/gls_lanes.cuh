@@ -587,8 +587,10 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
     B.pend[lane] = -1;
     B.lane_first[lane] = B.lane_last[lane] = -1;
     B.lev[lane] = B.levt[lane] = 0;
-    warp_aux_cold(p).lcyc[lane] = 0;
-    warp_aux_cold(p).lit[lane] = warp_aux_cold(p).lsu[lane] = 0;
+    if (p.trace) {
+        warp_aux_cold(p).lcyc[lane] = 0;
+        warp_aux_cold(p).lit[lane] = warp_aux_cold(p).lsu[lane] = 0;
+    }
     __syncwarp();
 
     for (;;) {
@@ -616,7 +618,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 // nothing but constants lives across the set-up call: the round's counts, the
                 // iteration and the scratch fill go through shared memory (set-up path only)
                 B.lev[lane] += l_cnt & 0xffffu;
-            warp_aux_cold(p).lit[lane] += (uint32_t)it;
+                if (p.trace) warp_aux_cold(p).lit[lane] += (uint32_t)it;
                 B.levt[lane] += l_cnt >> 16;
                 l_cnt = 0;
                 B.sv_it[lane] = (uint16_t)it;
@@ -626,10 +628,10 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 const bool fast = unit_begin(p, u, ui);
                 {
                     const unsigned long long dc = (unsigned long long)(clock64() - c_u0);
-                    warp_aux_cold(p).lcyc[lane] += dc;
+                    if (p.trace) warp_aux_cold(p).lcyc[lane] += dc;
                     if (lane == __ffs(__activemask()) - 1) B.acc[A_BAL + 4] += dc;   // warp-level: one pass
                 }
-                warp_aux_cold(p).lsu[lane] += 1;
+                if (p.trace) warp_aux_cold(p).lsu[lane] += 1;
                 it = B.sv_it[lane];
                 used = B.sv_used[lane];
                 if (!fast) {                                             // long delays: per-lane ring engine
@@ -764,7 +766,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         {
             const unsigned itmax = __reduce_max_sync(FULL, (unsigned)it), itsum = __reduce_add_sync(FULL, (unsigned)it);
             B.lev[lane] += l_cnt & 0xffffu;
-            warp_aux_cold(p).lit[lane] += (uint32_t)it;
+            if (p.trace) warp_aux_cold(p).lit[lane] += (uint32_t)it;
             B.levt[lane] += l_cnt >> 16;
             l_cnt = 0;
             if (lane == 0) {
@@ -835,7 +837,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
         __syncwarp();
     }
     const unsigned ev = __reduce_add_sync(FULL, B.lev[lane]), evt = __reduce_add_sync(FULL, B.levt[lane]);
-    const unsigned long long sc = warp_sum64(warp_aux_cold(p).lcyc[lane]);
+    const unsigned long long sc = p.trace ? warp_sum64(warp_aux_cold(p).lcyc[lane]) : 0ull;
     if (lane == 0) {
         B.acc[A_EVALS] += ev;
         B.acc[A_EVENTS] += evt;
@@ -958,18 +960,19 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         }
         // ---- static units: a chunk with at least w = total/32 expected entries is cut into
         // about est/w time slices, a smaller chunk is one unit
-        const unsigned long long w = max((unsigned long long)W_MIN, (total + 31) / 32);
+        // (32-bit arithmetic: a batch holds at most ~16 chunks of ~M expected entries)
+        const uint32_t w = (uint32_t)max((unsigned long long)W_MIN, min((total + 31) / 32, 0x3fffffffull));
         for (int j = 0; j < nc; ++j) {
-            const unsigned long long e = est[j];
-            int ns = e >= w && !B.c_inf[j] ? (int)min(32ull, max(1ull, (e + w / 2) / w)) : 1;
-            if (!B.c_inf[j]) ns = max(ns, (int)min(32ull, (e + U_MAX - 1) / U_MAX));
+            const uint32_t e = (uint32_t)min(est[j], 0x3fffffffull);
+            int ns = e >= w && !B.c_inf[j] ? (int)min(32u, max(1u, (e + w / 2) / w)) : 1;
+            if (!B.c_inf[j]) ns = max(ns, (int)min(32u, (e + (uint32_t)U_MAX - 1u) / (uint32_t)U_MAX));
             ns = max(1, min(ns, MAXU_STATIC - nu - (nc - 1 - j)));   // room for the later chunks
             B.c_first[j] = (uint8_t)nu;
             B.c_nsl[j] = (uint8_t)ns;
             for (int q = 0; q < ns; ++q, ++nu) {
                 B.u_chunk[nu] = (uint8_t)j;
                 B.u_slice[nu] = (uint8_t)q;
-                B.u_est[nu] = B.c_inf[j] ? 0u : (uint32_t)min(e / ns, 0xffffffffull);   // (0: never split)
+                B.u_est[nu] = B.c_inf[j] ? 0u : e / (uint32_t)ns;   // (0: never split)
                 B.u_next[nu] = q + 1 < ns ? (uint8_t)(nu + 1) : kEnd;
                 B.u_st[nu] = 0;
                 B.u_lane[nu] = 0;

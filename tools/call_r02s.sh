@@ -1,0 +1,5 @@
+set -u
+T=r02s
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_cells.py -m gpu -x -q --timeout 120 > gpurun_out/$T.pytest.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/$T.pytest.log
+export EXTRA=""
+bash tools/ab2.sh $T "default wm64 wm128 wm16" "c4_10m c3_1m c4_mini"
