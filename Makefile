@@ -14,13 +14,19 @@ $(PKG)/libgls.so: $(SRC) $(HDR)
 oracle/liboracle.so: oracle/gls_oracle.c
 	gcc -O2 -std=c11 -shared -fPIC -o $@ $<
 
+# bounds-checked build (device asserts on every hot-path access; tests: GLS_LIB=... pytest -m gpu)
+check: $(PKG)/libgls_check.so
+
+$(PKG)/libgls_check.so: $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -DGLS_CHECK -shared -o $@ $(SRC) -lcudart
+
 ptxas: $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -Xptxas -v -c -o /tmp/gls_kernels.o $(PKG)/csrc/gls_kernels.cu
 
 clean:
 	rm -f $(PKG)/libgls.so oracle/liboracle.so
 
-.PHONY: all clean ptxas
+.PHONY: all clean ptxas check
 
 # A/B variants for performance experiments (not used by tests)
 variant-%: $(SRC) $(HDR)

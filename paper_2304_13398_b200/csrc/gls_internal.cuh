@@ -12,7 +12,26 @@
 //             A gate's chunks are its (gate, time-chunk) work items.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
+
+// Bounds-checked build (make check -> libgls_check.so, -DGLS_CHECK): every store and load of
+// the hot path is checked against the buffer it must stay in; a violation prints the
+// condition and traps the kernel.  The stand-in for compute-sanitizer, which is closed on
+// the GPU pool (profiles/r02_sanitizer_closed.txt).
+#ifdef GLS_CHECK
+#define GLS_ASSERT(c)                                                                              \
+    do {                                                                                           \
+        if (!(c)) {                                                                                \
+            printf("GLS_CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c);                        \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define GLS_ASSERT(c) \
+    do {              \
+    } while (0)
+#endif
 
 namespace gls {
 

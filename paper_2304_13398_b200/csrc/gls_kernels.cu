@@ -173,6 +173,7 @@ __device__ long long time_at(const SimParams& p, uint32_t net, unsigned long lon
         if (__ldcg(&p.ck_cum[cb + mid]) <= idx) lo = mid; else hi = mid;
     }
     uint32_t j = cb + lo;
+    GLS_ASSERT(j < p.ck_cap && __ldcg(&p.ck_off[j]) + (idx - __ldcg(&p.ck_cum[j])) < p.arena_cap);
     return etime(p.arena[__ldcg(&p.ck_off[j]) + (idx - __ldcg(&p.ck_cum[j]))]);
 }
 
@@ -310,6 +311,7 @@ __device__ __noinline__ void run_chunk(const SimParams& p, const ChunkSetup& s, 
         if (rr < T0) {
             vb = (uint32_t)(e & 3u);
         } else if (rr < T1 && rr <= dur) {
+            GLS_ASSERT(!WRITE || (out + cnt >= p.arena && out + cnt < p.arena + p.arena_cap));
             if (WRITE) out[cnt] = e;
             ++cnt;
         }
@@ -342,6 +344,7 @@ __device__ __noinline__ void run_chunk(const SimParams& p, const ChunkSetup& s, 
                         if (hi - lo >= cap) {
                             overflow = true;
                         } else {
+                            GLS_ASSERT(!DEEP || (dbuf + (hi & mask) >= p.deep && dbuf + (hi & mask) < p.deep + p.deep_cap));
                             ring[hi & mask] = ((uint64_t)rr << 2) | E;
                             ++hi;
                         }
@@ -696,6 +699,7 @@ __device__ void plan_gate(const SimParams& p, uint32_t c) {
         fence_release();
     }
     // chunk start times: quantiles of the longest fan-in's transition times
+    GLS_ASSERT(base + nch <= p.ck_cap);
     for (unsigned long long j = lane; j < nch; j += 32) {
         const unsigned long long q = lenref / nch, rm = lenref % nch;
         p.ck_T[base + j] = j == 0 ? 0 : time_at(p, ref, j * q + (j * rm) / nch);
@@ -759,6 +763,8 @@ __device__ void chunk_done(const SimParams& p, unsigned long long id, const Chun
     const int lane = threadIdx.x & 31;
     unsigned prev = 0;
     if (lane == 0) {
+        GLS_ASSERT(id < p.ck_cap && R.gi < (uint32_t)p.G);
+        GLS_ASSERT(!R.fits || R.off + R.total <= p.arena_cap);
         if (R.fits) {
             p.ck_T[id] = R.s.T0;
             p.ck_off[id] = R.off;

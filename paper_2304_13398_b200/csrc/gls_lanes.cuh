@@ -162,8 +162,10 @@ __device__ __forceinline__ Seg next_segment(const SimParams& p, uint32_t ck, uin
     Seg r{nullptr, 0u, ck};
     while (r.rem == 0 && r.ck + 1 < ckend) {
         ++r.ck;
+        GLS_ASSERT(r.ck < p.ck_cap);
         r.ptr = p.arena + __ldcg(&p.ck_off[r.ck]);
         r.rem = __ldcg(&p.ck_cnt[r.ck]);
+        GLS_ASSERT(r.rem == 0 || __ldcg(&p.ck_off[r.ck]) + r.rem <= p.arena_cap);
     }
     return r;
 }
@@ -356,6 +358,8 @@ __device__ __forceinline__ void locate_all(const SimParams& p, const uint32_t* s
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const uint32_t j = cb[i] + lo[i];
+        GLS_ASSERT((uint32_t)i >= k || (j < p.ck_cap && j < c[i].ck_end &&
+                                        __ldcg(&p.ck_off[j]) + __ldcg(&p.ck_cnt[j]) <= p.arena_cap));
         seg[i] = (uint32_t)i < k ? p.arena + __ldcg(&p.ck_off[j]) : p.arena;
         cnt[i] = (uint32_t)i < k ? __ldcg(&p.ck_cnt[j]) : 0u;
         a[i] = 0;
@@ -690,6 +694,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 const int ci = b * kThreads + tid;
                 const uint64_t* ptr = (const uint64_t*)lds64(cs.ptr(ci)) + 1;
                 uint32_t rem = lds32(cs.rem(ci)) - 1u;
+                GLS_ASSERT(rem < 0x80000000u && ptr >= p.arena && ptr + rem <= p.arena + p.arena_cap);
                 cp_wait_pin(b, lastpin);                                 // the pin's lookahead has landed
                 uint64_t hn = lds64(cs.hn(ci));
                 if (rem == 0) {                                          // segment end: next non-empty segment
@@ -740,6 +745,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                     // (del = 0xFFFF: every changed pin is unrelated, nothing scheduled, R9)
                     const uint32_t fl = nfl & 0xffffu;
                     while (del != kDelayInf16 && n > fl && top >= rq) {
+                        GLS_ASSERT(n >= 1u && n <= (uint32_t)LCAP);
                         --n;
                         top = n > fl ? to_rel(ldg64(scr + n - 1), b4) : 0u;
                     }
@@ -747,6 +753,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                     if (tv != E && del != kDelayInf16) {                 // push unless it repeats the tail
                         if (n < (uint32_t)LCAP) {
                             top = rq | E;
+                            GLS_ASSERT(sbase + n < (uint32_t)(gridDim.x * (blockDim.x >> 5)) * 32u * (uint32_t)LCAP);
                             stg64(scr + n, (uint64_t)top + b4);
                             ++n;
                         } else {
@@ -812,6 +819,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
             const int rl = __ffs(rcv) - 1;
             rcv &= rcv - 1;
             if (lane == dl) {
+                GLS_ASSERT(nun < MAXU && u >= 0 && u < MAXU);
                 B.u_T0[nun] = ts;
                 B.u_T1[nun] = T1u;
                 B.u_chunk[nun] = B.u_chunk[u];
@@ -947,6 +955,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
                 break;
             }
             units_needed += need;
+            GLS_ASSERT(nc < MAXC && id < p.ck_cap && g < (uint32_t)p.G);
             B.c_inf[nc] = (p.gate[g].flags & kGateInf) != 0;
             B.id[nc] = id;
             warp_aux(p).c_t[nc] = p.trace ? gtimer() : 0ull;
@@ -970,6 +979,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             B.c_first[j] = (uint8_t)nu;
             B.c_nsl[j] = (uint8_t)ns;
             for (int q = 0; q < ns; ++q, ++nu) {
+                GLS_ASSERT(nu < MAXU_STATIC);
                 B.u_chunk[nu] = (uint8_t)j;
                 B.u_slice[nu] = (uint8_t)q;
                 B.u_est[nu] = B.c_inf[j] ? 0u : e / (uint32_t)ns;   // (0: never split)
@@ -1085,6 +1095,8 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             continue;
         }
         const uint64_t* src = p.wscr + (warp_global_id() * 32u + (uint32_t)lane) * (uint32_t)LCAP + __ldcg(&warp_aux(p).u_soff[v]);
+        GLS_ASSERT(off + __ldcg(&warp_aux(p).u_pre[v]) + cu <= p.arena_cap);
+        GLS_ASSERT(__ldcg(&warp_aux(p).u_soff[v]) + cu <= (uint32_t)LCAP);
         uint32_t e = 0;
         for (; e + 4 <= cu; e += 4) {
             const uint64_t a0 = src[e], a1 = src[e + 1], a2 = src[e + 2], a3 = src[e + 3];
