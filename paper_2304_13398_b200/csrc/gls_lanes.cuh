@@ -76,8 +76,11 @@ constexpr int MAXSPLIT = GLS_MAXSPLIT;           // splits per re-balancing poin
 #ifndef GLS_MAXSLEEP
 #define GLS_MAXSLEEP 8192                        // ns: longest back-off of a warp waiting for published work
 #endif
+#ifndef GLS_BATCH_AA
+#define GLS_BATCH_AA 32                          // backlog above which a busy warp claims more ids by
+#endif                                           // atomicAdd (0: compare-and-swap on a published head only)
 #ifndef GLS_ADAPT
-#define GLS_ADAPT 1                              // batch fill adapts to the queue depth (dataflow scheduler)
+#define GLS_ADAPT 0                              // 1: one chunk per batch when the queue is shallow (dataflow)
 #endif
 #ifndef GLS_ADAPT_FILL
 #define GLS_ADAPT_FILL 1                         // expected entries a shallow-queue batch is filled to
@@ -85,7 +88,10 @@ constexpr int MAXSPLIT = GLS_MAXSPLIT;           // splits per re-balancing poin
 #ifndef GLS_MAXU
 #define GLS_MAXU 64
 #endif
-constexpr int MAXC = 16;                         // chunks per batch
+#ifndef GLS_MAXC
+#define GLS_MAXC 16
+#endif
+constexpr int MAXC = GLS_MAXC;                   // chunks per batch
 constexpr int MAXU = GLS_MAXU;                   // units per batch (static + split)
 constexpr int MAXU_STATIC = MAXU * 5 / 8;        // static units per batch (the rest is room for splits)
 constexpr uint8_t kEnd = 0xff;
@@ -889,11 +895,19 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
                     id = atomicAdd(&p.ctl->work_head, 1ull);    // (an idle warp may wait for its id)
                 } else {
                     // a busy warp never holds an unpublished id (its consumers would wait for
-                    // this whole batch): take the head only if published, by compare-and-swap
+                    // this whole batch): take the head only if published, by compare-and-swap —
+                    // or, with a backlog of allocated ids ahead of the head (GLS_BATCH_AA), by
+                    // atomicAdd (such ids are published moments after their allocation; one
+                    // that is not yet is carried to the next batch)
                     const unsigned long long h = ld_relaxed_u64(&p.ctl->work_head);
-                    if (h >= p.ck_cap || ld_relaxed_u32(&p.ck_gate[h]) == 0xffffffffu) break;
-                    if (atomicCAS(&p.ctl->work_head, h, h + 1ull) != h) break;
-                    id = h;
+                    if (GLS_BATCH_AA > 0 &&
+                        ld_relaxed_u64(&p.ctl->chunk_top) > h + (unsigned long long)GLS_BATCH_AA) {
+                        id = atomicAdd(&p.ctl->work_head, 1ull);
+                    } else {
+                        if (h >= p.ck_cap || ld_relaxed_u32(&p.ck_gate[h]) == 0xffffffffu) break;
+                        if (atomicCAS(&p.ctl->work_head, h, h + 1ull) != h) break;
+                        id = h;
+                    }
                 }
             } else {
                 const unsigned long long w = atomicAdd(lvl_work, 1ull);

@@ -64,3 +64,22 @@ for g in slow:
     print(f"slowest chunk: gate {g} level {glev[g]} n_in {n_in[g]:.0f} max chunk {cmax[g]:.0f} us, "
           f"sum {csum[g]:.0f} us, planned {plan[g]:.0f} us, done {done[g]:.0f} us, batch rounds {crounds[g]} "
           f"units {cunits[g]} busiest lane {cmaxit[g]} iterations, most set-ups {cmaxsu[g]}")
+# critical path: from the last gate to complete, walk back through the fan-in gate that
+# completed last (the one whose completion planned it); per step: wait (plan - that
+# fan-in's done) and run (done - plan) of the gate
+g = int(np.argmax(done))
+path = []
+while True:
+    path.append(g)
+    a, b = nl.fanin_offsets[g], nl.fanin_offsets[g + 1]
+    srcs = [int(x) - P for x in nl.fanin_net[a:b] if x >= P]
+    if not srcs:
+        break
+    g = max(srcs, key=lambda x: done[x])
+path = path[::-1]
+run = sum(done[x] - plan[x] for x in path)
+print(f"critical path: {len(path)} gates, levels {glev[path[0]]}..{glev[path[-1]]}, ends at {done[path[-1]]:.0f} us; "
+      f"running {run:.0f} us, waiting {done[path[-1]] - run:.0f} us; first planned at {plan[path[0]]:.0f} us")
+for x in path[:: max(1, len(path) // 15)]:
+    print(f"  gate {x} level {glev[x]} n_in {n_in[x]:.0f} planned {plan[x]:.0f} done {done[x]:.0f} "
+          f"(run {done[x] - plan[x]:.0f} us, max chunk {cmax[x]:.0f} us)")
