@@ -81,7 +81,7 @@ typedef struct gls_config {
                                 free HBM)                     */
     int64_t chunk_capacity;  /* max (gate, time-chunk) work items per run; 0 = auto */
     int32_t chunk_events;    /* target merged input events per work item (M);
-                                0 = 65536 / 256 for engines 0 / 1                  */
+                                0 = 32768 / 256 for engines 0 / 1                  */
     int32_t blocks_per_sm;   /* persistent-kernel CTAs per SM; 0 = max co-resident */
     int32_t ring_limit;      /* TESTING: cap on the on-chip pending-schedule ring
                                 (1..32) to force the deep-backtrace path; 0 = 32 */

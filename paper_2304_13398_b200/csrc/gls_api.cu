@@ -217,7 +217,7 @@ int64_t free_bytes(gls_ctx* ctx) {
     return (int64_t)fr;
 }
 
-int default_M(int engine) { return engine == 0 ? 65536 : 256; }
+int default_M(int engine) { return engine == 0 ? 32768 : 256; }
 
 SimParams params(gls_ctx* ctx) {
     SimParams p{};

@@ -79,6 +79,9 @@ constexpr int MAXSPLIT = GLS_MAXSPLIT;           // splits per re-balancing poin
 #ifndef GLS_BATCH_AA
 #define GLS_BATCH_AA 32                          // backlog above which a busy warp claims more ids by
 #endif                                           // atomicAdd (0: compare-and-swap on a published head only)
+#ifndef GLS_ALONE
+#define GLS_ALONE 4096                           // chunks of at least this many expected entries form a batch alone
+#endif
 #ifndef GLS_ADAPT
 #define GLS_ADAPT 0                              // 1: one chunk per batch when the queue is shallow (dataflow)
 #endif
@@ -964,7 +967,11 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             // static units of at most U_MAX expected entries (a unit's outputs must fit the lane
             // scratch); a chunk that would not fit the batch's unit budget waits for the next batch
             const int need = (int)min(32ull, max(1ull, (e + U_MAX - 1) / U_MAX));
-            if (nc > 0 && units_needed + need > MAXU_STATIC) {
+            // a big chunk travels alone (GLS_ALONE: at least this many expected entries):
+            // small chunks batched with it would complete only when it does, and one of them
+            // may be on the critical path
+            const bool big = GLS_ALONE > 0 && e >= (unsigned long long)GLS_ALONE;
+            if (nc > 0 && (units_needed + need > MAXU_STATIC || big)) {
                 carry = id;
                 break;
             }
@@ -976,6 +983,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
             est[nc] = e;
             total += e;
             ++nc;
+            if (big) break;
         }
         if (nc > 0) {
             B.acc[A_BATCHES] += 1ull;
