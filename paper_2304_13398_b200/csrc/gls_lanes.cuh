@@ -59,6 +59,10 @@ constexpr int W_MIN = GLS_WMIN;                  // fewest expected entries per 
 #define GLS_ROUND 512
 #endif
 constexpr int ROUND = GLS_ROUND;                 // sweep iterations between re-balancing points
+#ifndef GLS_ROUND_BIG
+#define GLS_ROUND_BIG 512
+#endif
+constexpr int ROUND_BIG = GLS_ROUND_BIG;         // the same for a batch of one big chunk (>= GLS_ALONE)
 #ifndef GLS_MQ_MIN
 #define GLS_MQ_MIN 0                             // chunks with at least this many expected entries are
 #endif                                           // sliced at merged-count quantiles (0: never)
@@ -199,6 +203,7 @@ struct Batch {
     int round;                             // re-balancing rounds of the batch so far
     uint16_t u_r0[MAXU];                   // round in which the unit started
     int nun;                               // units (static + split)
+    int big;                               // the batch is one big chunk (GLS_ALONE)
     int8_t pend[32];                       // unit handed to a lane by a split (-1: none)
     uint32_t lev[32], levt[32];            // per-lane gate-evals / events of the batch
     uint16_t sv_it[32];                    // (set-up call: the lane's round iteration,
@@ -578,6 +583,7 @@ __device__ __forceinline__ uint32_t unit_src(const SimParams& p, const Batch& B,
 // competes for registers.  Statistics go to B.acc (lane 0).
 __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
     Batch& B = warp_batch();
+    const int rlen = B.big ? ROUND_BIG : ROUND;
     const PinSm cs = pin_cols();
     const int lane = threadIdx.x & 31;
     const int tid = threadIdx.x;
@@ -608,7 +614,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
 
     for (;;) {
         int it = 0;
-        for (; it < ROUND; ++it) {
+        for (; it < rlen; ++it) {
             uint32_t tq;
             if (u < 0) {
                 // ---- take a unit: handed over by a split, else the next static one
@@ -812,7 +818,7 @@ __device__ __noinline__ void sweep_rounds(const SimParams& p, int nstatic) {
                 // an estimate from the chunk average misses bursts inside the unit
                 const float left = (float)(T1u - tn);
                 const float est = (float)B.u_est[u] * left / (float)max(1ll, T1u - T0u);
-                const float done = ((float)(B.round - (int)B.u_r0[u]) + 0.5f) * (float)ROUND;
+                const float done = ((float)(B.round - (int)B.u_r0[u]) + 0.5f) * (float)rlen;
                 re = fmaxf(est, done * left / (float)max(1ll, tn - T0u));
                 ts = tn + (T1u - tn) / 2;                                 // > every timestamp applied so far
             }
@@ -1012,6 +1018,7 @@ __device__ bool lane_batch(const SimParams& p, unsigned long long& carry, unsign
         }
         B.qhead = 0;
         B.round = 0;
+        B.big = GLS_ALONE > 0 && nc == 1 && est[0] >= (unsigned long long)GLS_ALONE;
         B.acc[A_BAL + 0] += (unsigned long long)nu;
         B.acc[A_BLANES] += (unsigned long long)min(nu, 32);
         p.deep_wtop[warp_global_id()] = 0;          // this warp's deep scratch, reused per batch
