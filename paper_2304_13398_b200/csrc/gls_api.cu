@@ -737,12 +737,21 @@ static int upload_and_validate(gls_ctx* ctx, int32_t P, const int64_t* off, cons
     DevBuf<uint64_t> st_tr;
     const long long* v_off = (const long long*)off;     // what is validated (device)
     const uint64_t* v_tr = tr;
-    bool in_place = false;
+    bool in_place = false, staged_in_arena = false;
     if (kind == cudaMemcpyHostToDevice) {
         CK(st_off.alloc((size_t)P + 1));
         CK(cudaMemcpyAsync(st_off.p, off, sizeof(int64_t) * (P + 1), kind, ctx->stream));
         v_off = st_off.p;
-        if (total) {
+        // staging room inside the arena, past everything the context still owns (given
+        // waveforms and the last result) and past where the new ones will go: no cudaMalloc /
+        // cudaFree of a stimulus-sized buffer per call
+        const int64_t owned = std::max<int64_t>(ctx->prefix_total, ctx->has_result ? (int64_t)ctx->last.arena_top : 0);
+        const int64_t at = (std::max<int64_t>(owned, total) + 15) & ~15ll;
+        if (total && ctx->d_arena.p && ctx->cfg.engine != 2 && at + total <= (int64_t)ctx->d_arena.n) {
+            CK(cudaMemcpyAsync(ctx->d_arena.p + at, tr, sizeof(uint64_t) * total, kind, ctx->stream));
+            v_tr = ctx->d_arena.p + at;
+            staged_in_arena = true;
+        } else if (total) {
             if (st_tr.alloc((size_t)total) != cudaSuccess) {
                 cudaGetLastError();
                 in_place = true;                        // no room for a staging copy
@@ -781,8 +790,10 @@ static int upload_and_validate(gls_ctx* ctx, int32_t P, const int64_t* off, cons
         ctx->has_inputs = ctx->has_result = false;
         ctx->window_active = false;
         ctx->prefix_total = 0;                          // nothing to keep while the arena is (re)sized
-        int rc = ensure_arena(ctx, total + 1, false);
-        if (rc) return rc;
+        if (!staged_in_arena) {                         // (staged in the arena: it already holds 2 x total)
+            int rc = ensure_arena(ctx, total + 1, false);
+            if (rc) return rc;
+        }
         if (total) CK(cudaMemcpyAsync(ctx->d_arena.p, v_tr, sizeof(uint64_t) * total, cudaMemcpyDeviceToDevice, ctx->stream));
     }
     CK(ctx->d_in_off.ensure((size_t)P + 1));
