@@ -36,7 +36,12 @@ import torch  # noqa: E402
 from paper_2304_13398_b200 import workloads as W  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
-C5_SETS = 64                # BASELINE configs[4]: 64 independent stimulus sets on the 1M-gate netlist
+C5_SETS = int(os.environ.get("GLS_BENCH_C5_SETS", "64"))   # BASELINE configs[4]: 64 independent stimulus sets
+# Functional multi-rank runs on ONE GPU (not measurements): GLS_BENCH_BACKEND=gloo stages the
+# collectives through host memory and GLS_BENCH_ONE_GPU=1 puts every rank on cuda:0 (NCCL
+# refuses two ranks on one device).  The product path is NCCL, one rank per GPU.
+BACKEND = os.environ.get("GLS_BENCH_BACKEND", "nccl")
+ONE_GPU = os.environ.get("GLS_BENCH_ONE_GPU", "0") == "1"
 
 # prefix of the workload the oracle runs (cycles), sized for ~10-30 s of one core
 SAMPLE_CYCLES = {"c4_10m": 3000, "c3_1m": 60, "c7552": 1999, "c5_set": 150, "c4_mini": 3000}
@@ -63,6 +68,11 @@ def parse():
     ap.add_argument("--wcv", type=float, default=0.0,
                     help="A/B only: override the skewed profile's WCV target (Eq. 5) of the config")
     return ap.parse_args()
+
+
+def _shard_ag(out, t):
+    from paper_2304_13398_b200 import shard
+    shard.all_gather_t(out, t)
 
 
 def log(*a):
@@ -250,11 +260,11 @@ def post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_ha
         st_ms = s0.elapsed_time(s1)
         tt = torch.tensor([st_ms], dtype=torch.float64, device=dev)
         allv = [torch.zeros_like(tt) for _ in range(world)]
-        torch.distributed.all_gather(allv, tt)
+        _shard_ag(allv, tt)
         stitch = {"ms": float(torch.stack(allv).max()), "nets": int(stitched.numel()),
                   "bytes_per_rank": int(16 * stitched.numel()),
                   "what": "full-run per-net checksums from the time windows (all_gather of counts and "
-                          "position-keyed terms over NCCL)"}
+                          f"position-keyed terms over {BACKEND})"}
         del stitched
         # the waveforms themselves (§8(e) stitch): every rank's owned-window CSR of the first
         # 1/16 of the nets to rank 0 (the whole result, ~90 GB, would not fit beside rank 0's
@@ -269,12 +279,12 @@ def post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_ha
         g_ms = s0.elapsed_time(s1)
         tt = torch.tensor([g_ms], dtype=torch.float64, device=dev)
         allv = [torch.zeros_like(tt) for _ in range(world)]
-        torch.distributed.all_gather(allv, tt)
+        _shard_ag(allv, tt)
         if rank == 0:
             g_bytes = 8 * int(res[0][-1])
             stitch["waveforms"] = {"ms": float(torch.stack(allv).max()), "nets": [0, n_sub], "bytes": g_bytes,
                                    "gbs": g_bytes / (float(torch.stack(allv).max()) / 1e3) / 1e9,
-                                   "what": "owned-window CSRs (gls_get_waveforms_range_device) -> NCCL "
+                                   "what": f"owned-window CSRs (gls_get_waveforms_range_device) -> {BACKEND} "
                                            "send/recv to rank 0 -> gls_scatter_segments into the full-run CSR"}
         del res
     if world > 1 and replicas:
@@ -287,13 +297,13 @@ def post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_ha
         mine = torch.zeros((per, nl.num_nets), dtype=torch.int64, device=dev)
         mine[:len(stims)] = set_hashes
         allh = [torch.empty_like(mine) for _ in range(world)]
-        torch.distributed.all_gather(allh, mine)
+        _shard_ag(allh, mine)
         s1.record(stream)
         torch.cuda.synchronize(dev)
         # set k lives on rank k % world at row k // world
         h0 = allh[0][0].cpu()
         stitch = {"ms": s0.elapsed_time(s1), "sets": C5_SETS, "bytes": int(8 * per * world * nl.num_nets),
-                  "what": "per-set per-net checksums (device, in the step) all_gathered over NCCL",
+                  "what": f"per-set per-net checksums (device, in the step) all_gathered over {BACKEND}",
                   "set0_matches_rank0": bool(torch.equal(h0, set_hashes[0].cpu()))}
         del allh, mine
     return stitch
@@ -302,11 +312,16 @@ def post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_ha
 def run_gls(a):
     from paper_2304_13398_b200 import gls
     rank, world, local = dist_env()
+    if ONE_GPU:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(BACKEND)
     cfg = a.config
     nl = build_netlist(cfg, a.seed)
     # C5 (BASELINE configs[4]): C5_SETS independent stimulus sets on one netlist, dealt
@@ -400,7 +415,7 @@ def run_gls(a):
         import torch.distributed as dist
         tt = torch.tensor([ms, kms, units, outs, alg], dtype=torch.float64, device=dev)
         allv = [torch.zeros_like(tt) for _ in range(world)]
-        dist.all_gather(allv, tt)
+        _shard_ag(allv, tt)
         allv = torch.stack(allv).cpu().numpy()
         ms, kms = float(allv[:, 0].max()), float(allv[:, 1].max())
         units, outs = float(allv[:, 2].sum()), float(allv[:, 3].sum())
@@ -445,7 +460,7 @@ def run_gls(a):
             import torch.distributed as dist
             tt = torch.tensor([e_ms, e_units], dtype=torch.float64, device=dev)
             allv = [torch.zeros_like(tt) for _ in range(world)]
-            dist.all_gather(allv, tt)
+            _shard_ag(allv, tt)
             allv = torch.stack(allv).cpu().numpy()
             e_ms, e_units = float(allv[:, 0].max()), float(allv[:, 1].sum())
         e2e = {"value": e_units / (e_ms / 1e3), "unit": "gate-evals/s",

@@ -44,12 +44,47 @@ def rank_plan(rank: int, world: int, ncycles: int, halo_ps: int, duration: int):
     return {"gen_cycles": (max(0, k_lo - look), k_hi), "duration": sim_dur, "own": (own_lo, own_hi)}
 
 
+def _host_staged(group=None) -> bool:
+    """gloo moves CPU tensors only: device tensors are staged through host memory (used by
+    the functional multi-rank runs on one GPU; NCCL, the product backend, takes them as they
+    are)."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def all_gather_t(out, t, group=None):
+    """dist.all_gather into the list `out` (tensors like t), any device."""
+    import torch.distributed as dist
+    if _host_staged(group) and t.is_cuda:
+        oc = [torch.empty(o.shape, dtype=o.dtype) for o in out]
+        dist.all_gather(oc, t.cpu(), group=group)
+        for o, c in zip(out, oc):
+            o.copy_(c)
+    else:
+        dist.all_gather(out, t, group=group)
+
+
+def send_t(t, dst, group=None):
+    import torch.distributed as dist
+    dist.send(t.cpu() if _host_staged(group) and t.is_cuda else t, dst, group=group)
+
+
+def recv_t(t, src, group=None):
+    import torch.distributed as dist
+    if _host_staged(group) and t.is_cuda:
+        c = torch.empty(t.shape, dtype=t.dtype)
+        dist.recv(c, src, group=group)
+        t.copy_(c)
+    else:
+        dist.recv(t, src, group=group)
+
+
 def all_gather_rows(values, device, group=None):
     """all_gather a small float64 vector from every rank -> [world, len] CPU tensor."""
     import torch.distributed as dist
     t = torch.as_tensor(values, dtype=torch.float64, device=device)
     out = [torch.zeros_like(t) for _ in range(dist.get_world_size(group))]
-    dist.all_gather(out, t, group=group)
+    all_gather_t(out, t, group=group)
     return torch.stack(out).cpu()
 
 
@@ -64,13 +99,13 @@ def stitch_hashes(counts, terms_fn, group=None):
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     allc = [torch.empty_like(counts) for _ in range(world)]
-    dist.all_gather(allc, counts, group=group)
+    all_gather_t(allc, counts, group=group)
     allc = torch.stack(allc)
     base = allc[:rank].sum(0) if rank > 0 else torch.zeros_like(counts)
     total = allc.sum(0) if rank == 0 else None
     terms = terms_fn(base, total)
     allt = [torch.empty_like(terms) for _ in range(world)]
-    dist.all_gather(allt, terms, group=group)
+    all_gather_t(allt, terms, group=group)
     h = allt[0].clone()
     for t in allt[1:]:
         h.bitwise_xor_(t)
@@ -126,12 +161,12 @@ def stitch_waveforms(counts, buf, scatter_fn, out_alloc, dst=0, group=None):
     import torch.distributed as dist
     world, rank = dist.get_world_size(group), dist.get_rank(group)
     allc = [torch.empty_like(counts) for _ in range(world)]
-    dist.all_gather(allc, counts, group=group)
+    all_gather_t(allc, counts, group=group)
     allc = torch.stack(allc)
     sizes = allc.sum(1).tolist()
     if rank != dst:
         if sizes[rank]:
-            dist.send(buf[:sizes[rank]].contiguous(), dst, group=group)
+            send_t(buf[:sizes[rank]].contiguous(), dst, group=group)
         return None
     bufs = []
     for r in range(world):
@@ -140,7 +175,7 @@ def stitch_waveforms(counts, buf, scatter_fn, out_alloc, dst=0, group=None):
         else:
             b = torch.empty(max(1, sizes[r]), dtype=torch.int64, device=counts.device)
             if sizes[r]:
-                dist.recv(b[:sizes[r]], r, group=group)
+                recv_t(b[:sizes[r]], r, group=group)
             bufs.append(b)
     return assemble(allc, bufs, scatter_fn, out_alloc)
 
