@@ -527,6 +527,29 @@ CONFIGS = {
 }
 
 
+def union_netlist(nl: Netlist, k: int) -> Netlist:
+    """k disjoint copies of a netlist as one (independent stimulus sets simulated in one
+    launch).  Nets: the copies' given nets first (copy c's net p -> c*P + p), then the
+    copies' gates (copy c's gate g -> k*P + c*G + g); see union_nets."""
+    if k == 1:
+        return nl
+    P, G, E = nl.num_inputs, nl.num_gates, nl.num_pins
+    fo = nl.fanin_offsets.astype(np.int64)
+    src = nl.fanin_net.astype(np.int64)
+    offs, nets = [np.zeros(1, np.int64)], []
+    for c in range(k):
+        offs.append(fo[1:] + c * E)
+        nets.append(np.where(src < P, src + c * P, k * P + c * G + (src - P)))
+    return Netlist(k * P, np.tile(nl.gate_type, k), np.concatenate(offs),
+                   np.concatenate(nets).astype(np.int32), np.tile(nl.pin_delay, (k, 1)))
+
+
+def union_nets(nl: Netlist, k: int, c: int) -> np.ndarray:
+    """user net ids, in the single netlist's net order, of copy c inside union_netlist(nl, k)"""
+    P, G = nl.num_inputs, nl.num_gates
+    return np.concatenate([c * P + np.arange(P), k * P + c * G + np.arange(G)]).astype(np.int64)
+
+
 def config_netlist(name: str, seed: int = 1) -> Netlist:
     c = CONFIGS[name]
     return recipe_netlist(seed, c["num_gates"], c["depth"], c["num_inputs"])

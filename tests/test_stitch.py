@@ -98,3 +98,26 @@ def test_stitch_waveforms_gloo(world):
     full = _full(nl, spec)
     assert np.array_equal(off, full.offsets)
     assert np.array_equal(tr, full.trans)
+
+
+def test_union_netlist_is_its_copies():
+    """C5's batching of independent stimulus sets (bench.py --c5-union): k disjoint copies of
+    a netlist simulated as one, each copy driven by its own set, give every copy exactly the
+    single-set result (oracle on both sides)."""
+    nl = W.recipe_netlist(5, 300, 12, 20)
+    k = 3
+    u = W.union_netlist(nl, k)
+    sts = [W.random_stimuli(40 + c, nl.num_inputs, 30, 600, xz=0.1) for c in range(k)]
+    off = [np.zeros(1, np.int64)]
+    tr, base = [], 0
+    for st in sts:
+        off.append(st.offsets[1:] + base)
+        base += int(st.offsets[-1])
+        tr.append(st.trans)
+    ust = W.Stimuli(np.concatenate(off), np.concatenate(tr).astype(np.uint64))
+    ref = oracle.simulate(u.num_inputs, u.gate_type, u.fanin_offsets, u.fanin_net, u.pin_delay,
+                          ust.offsets, ust.trans, 650)
+    for c, st in enumerate(sts):
+        one = oracle.simulate(nl.num_inputs, nl.gate_type, nl.fanin_offsets, nl.fanin_net, nl.pin_delay,
+                              st.offsets, st.trans, 650)
+        assert np.array_equal(ref.hashes[W.union_nets(nl, k, c)], one.hashes)
