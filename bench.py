@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--arena-gb", type=float, default=0.0)
     ap.add_argument("--engine", type=int, default=0)
     ap.add_argument("--scheduler", type=int, default=0)
+    ap.add_argument("--c5-union", type=int, default=8,
+                    help="C5: stimulus sets per launch (k disjoint netlist copies, one set each)")
     ap.add_argument("--ncycles", type=int, default=0,
                     help="A/B / profiling only: override the config's number of clock cycles")
     ap.add_argument("--wcv", type=float, default=0.0,
@@ -295,7 +297,7 @@ def post_timing_stitch(ctx, nl, plan, dev, stream, world, rank, replicas, set_ha
         s0.record(stream)
         per = (C5_SETS + world - 1) // world
         mine = torch.zeros((per, nl.num_nets), dtype=torch.int64, device=dev)
-        mine[:len(stims)] = set_hashes
+        mine[:set_hashes.shape[0]] = set_hashes
         allh = [torch.empty_like(mine) for _ in range(world)]
         _shard_ag(allh, mine)
         s1.record(stream)
@@ -330,12 +332,21 @@ def run_gls(a):
     sets = list(range(rank, C5_SETS, world)) if cfg == "c5_set" else [0]
     replicas = cfg == "c5_set"
     spec = W.config_stimspec(cfg, a.seed + sets[0])
+    # C5: UK sets per launch, as UK disjoint copies of the netlist (independent problems in
+    # one launch fill the warps a single set's critical path leaves idle; each copy's result
+    # is exactly its set's, tests/test_stitch.py::test_union_netlist_is_its_copies)
+    UK = 1
+    if replicas:
+        UK = max(1, min(a.c5_union, len(sets)))
+        while len(sets) % UK:
+            UK -= 1
+    unl = W.union_netlist(nl, UK)
     stream = torch.cuda.current_stream(dev)
     ctx = gls.Context(local, stream.cuda_stream)
     ctx.gls_set_config(chunk_events=a.chunk_events, blocks_per_sm=a.blocks_per_sm,
                        arena_bytes=int(a.arena_gb * (1 << 30)), engine=a.engine, scheduler=a.scheduler)
     t = time.perf_counter()
-    ctx.load(nl)
+    ctx.load(unl)
     L = ctx.gls_get_levels()
     H = ctx.gls_get_halo()
     log(f"loaded: {L} levels, halo {H} ps ({time.perf_counter() - t:.1f}s)")
@@ -347,35 +358,44 @@ def run_gls(a):
     k_hi = plan["gen_cycles"][1]
     duration = plan["duration"]
     t = time.perf_counter()
-    stims = []                       # this rank's given waveforms, resident in HBM: one per set
-    for k in sets:
-        sp = W.config_stimspec(cfg, a.seed + k) if replicas else spec
-        d_off, d_tr = W.window_stimuli(sp, *plan["gen_cycles"], dev)
+    stims = []                       # this rank's given waveforms, resident in HBM: one per launch
+    for g0 in range(0, len(sets), UK):
+        offs, trs, base = [], [], 0
+        for k in sets[g0:g0 + UK]:
+            sp = W.config_stimspec(cfg, a.seed + k) if replicas else spec
+            d_off, d_tr = W.window_stimuli(sp, *plan["gen_cycles"], dev)
+            offs.append(d_off if not offs else d_off[1:] + base)
+            base += int(d_tr.numel())
+            trs.append(d_tr)
+        d_off = offs[0] if UK == 1 else torch.cat(offs)
+        d_tr = trs[0] if UK == 1 else torch.cat(trs)
+        del offs, trs
         stims.append((d_off, d_tr, int(d_tr.numel())))
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()            # the generator's temporaries: leave the HBM to the library's arena
     d_off, d_tr, n_in = stims[0]
-    lens = (d_off[1:] - d_off[:-1]).double()
+    lens = (d_off[1:nl.num_inputs + 1] - d_off[:nl.num_inputs]).double()   # (set 0)
     wcv = float(lens.std(unbiased=False) / lens.mean()) if n_in else 0.0
     n_in_all = sum(x[2] for x in stims)
     log(f"stimuli: {len(stims)} set(s), {n_in_all} transitions on {spec.num_inputs} PIs, WCV {wcv:.2f} "
         f"({time.perf_counter() - t:.1f}s)")
-    if len(stims) == 1:
-        ctx.gls_set_input_waveforms_device(nl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), n_in)
-    set_hashes = torch.zeros((len(stims), nl.num_nets), dtype=torch.int64, device=dev) if len(stims) > 1 else None
+    if not replicas:
+        ctx.gls_set_input_waveforms_device(unl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), n_in)
+    # per launch: the checksums of every net of the (union) netlist, kept on the device
+    launch_hashes = torch.zeros((len(stims), unl.num_nets), dtype=torch.int64, device=dev) if replicas else None
 
     def step():
         """One pass of the hot path over the rank's batch of input: its time window, or each
         of its stimulus sets (set the device-resident inputs, simulate).  Returns the
         per-simulation stats of the step (kernel time, counts)."""
-        if len(stims) == 1:
+        if not replicas:
             ctx.gls_simulate(duration)
             return [ctx.gls_get_stats()]
         out = []
         for k_, (o_, t_, n_) in enumerate(stims):
-            ctx.gls_set_input_waveforms_device(nl.num_inputs, o_.data_ptr(), t_.data_ptr(), n_)
+            ctx.gls_set_input_waveforms_device(unl.num_inputs, o_.data_ptr(), t_.data_ptr(), n_)
             ctx.gls_simulate(duration)
-            ctx.gls_get_net_hashes_device(set_hashes[k_].data_ptr())     # a10 per set, on the device
+            ctx.gls_get_net_hashes_device(launch_hashes[k_].data_ptr())  # a10 per launch, on the device
             out.append(ctx.gls_get_stats())
         return out
 
@@ -421,6 +441,12 @@ def run_gls(a):
         units, outs = float(allv[:, 2].sum()), float(allv[:, 3].sum())
         alg = float(allv[:, 4].mean())                      # per launch on one GPU (roofline is per GPU)
 
+    # per-set checksums (each set's nets inside its launch's union netlist), after the timing
+    set_hashes = None
+    if launch_hashes is not None:
+        idx = [torch.as_tensor(W.union_nets(nl, UK, c), device=dev) for c in range(UK)]
+        set_hashes = torch.stack([launch_hashes[j][idx[c]] for j in range(len(stims)) for c in range(UK)])
+
     # N > 1 time windows: stitch the full-run per-net checksums from the ranks' windows
     # (NCCL all_gather of per-net counts, then of position-keyed terms; shard.stitch_hashes),
     # timed on the device after the timed region, max over ranks
@@ -449,7 +475,7 @@ def run_gls(a):
         e0.record(stream)
         for _ in range(n_e2e):
             for h_off, h_tr in pinned:
-                ctx.gls_set_input_waveforms(nl.num_inputs, h_off.numpy(), h_tr.numpy().view(np.uint64))
+                ctx.gls_set_input_waveforms(unl.num_inputs, h_off.numpy(), h_tr.numpy().view(np.uint64))
                 ctx.gls_simulate(duration)
                 hashes = ctx.gls_get_net_hashes()
         e1.record(stream)
@@ -467,7 +493,7 @@ def run_gls(a):
                "h2d_bytes_per_step": int(sum(8 * (o_.numel() + n_) for o_, _, n_ in e_sets)),
                "d2h_bytes_per_step": int(8 * hashes.size * len(e_sets)), "ms_per_step": e_ms,
                "api": "gls_set_input_waveforms(host pinned) + gls_simulate + gls_get_net_hashes" +
-                      (f", first {len(e_sets)} of the rank's {len(stims)} stimulus sets" if len(stims) > 1 else "")}
+                      (f", first {len(e_sets)} of the rank's {len(stims)} launches of {UK} stimulus sets" if replicas else "")}
         del pinned
 
     # e2e with a WAVEFORM readback (a10): each step H2D of the given waveforms (pinned), simulate,
@@ -475,7 +501,7 @@ def run_gls(a):
     # gathered on the device (gls_get_waveforms_range_device) and read back into pinned host
     # memory — the transitions themselves, not their checksums
     e2e_w = None
-    if not a.no_e2e and len(stims) == 1 and world == 1:
+    if not a.no_e2e and not replicas and world == 1:
         try:
             o_, t_, n_ = stims[0]
             h_off = torch.empty(o_.numel(), dtype=torch.int64, pin_memory=True)
@@ -533,8 +559,8 @@ def run_gls(a):
         else:
             readback = {"skipped": f"{need / 1e9:.0f} GB result > 40 % of the host's available memory"}
 
-    if len(stims) > 1:          # the parity check below is on the first set: simulate it again
-        ctx.gls_set_input_waveforms_device(nl.num_inputs, stims[0][0].data_ptr(), stims[0][1].data_ptr(), stims[0][2])
+    if replicas:                # the parity check below is on the first set: simulate it again
+        ctx.gls_set_input_waveforms_device(unl.num_inputs, stims[0][0].data_ptr(), stims[0][1].data_ptr(), stims[0][2])
         ctx.gls_simulate(duration)
 
     # CPU oracle on a bounded prefix of the same workload + full-size parity there
@@ -546,7 +572,7 @@ def run_gls(a):
                "sample": f"{cfg} netlist ({nl.num_gates} gates), first {cyc} of {nc} clock cycles "
                          f"(t <= {tmax} ps): {r.gate_evals} gate-evals in {dt:.2f} s, single thread",
                **host_cpu()}
-        gh = ctx.gls_get_net_hashes_window(0, tmax)
+        gh = ctx.gls_get_net_hashes_window(0, tmax)[W.union_nets(nl, UK, 0)]   # (set 0: copy 0)
         mism = int((gh != r.hashes).sum())
         parity = {"window_ps": [0, tmax], "nets": int(gh.size), "hash_mismatches": mism,
                   "bit_exact": mism == 0}
@@ -584,7 +610,7 @@ def run_gls(a):
                        "pis": nl.num_inputs, "pins": nl.num_pins,
                        "levels": L, "duration_ps": spec.duration, "stimulus_transitions": n_in,
                        "stimulus_wcv": round(wcv, 2), "halo_ps": H,
-                       **({"stimulus_sets": C5_SETS, "sets_per_rank": len(stims),
+                       **({"stimulus_sets": C5_SETS, "sets_per_rank": len(sets), "sets_per_launch": UK,
                            "stimulus_transitions_per_rank": n_in_all} if replicas else {}),
                        "parallelism": (f"stimulus sets round-robin over {world} rank(s), no exchange" if replicas else
                                        f"time-windows x{world}" if world > 1 else "single GPU"),
@@ -598,7 +624,7 @@ def run_gls(a):
             # per step: init_given_kernel + sim_kernel (gls_simulate) and fanin_reads_kernel
             # (gls_get_stats' algorithmic-bytes count, read after every step for kernel_ms)
             # (C5: + validate_kernel of gls_set_input_waveforms_device per set)
-            "gpu_launches": a.steps * len(stims) * (3 + (1 if len(stims) > 1 else 0)),
+            "gpu_launches": a.steps * len(stims) * (3 + (1 if replicas else 0)),   # (per launch)
             "clocks": ck,
         }
         print(json.dumps(line), flush=True)

@@ -132,3 +132,27 @@ def test_gather_waveforms_over_nccl_single_rank(ctx):
         dist.destroy_process_group()
     assert np.array_equal(off.cpu().numpy(), ref.offsets)
     assert np.array_equal(out[:int(off[-1])].cpu().numpy().view(np.uint64), ref.trans)
+
+
+def test_union_netlist_on_gpu_is_its_copies():
+    """bench.py's C5 batching on the GPU: k disjoint netlist copies, one stimulus set each,
+    in one gls_simulate give every copy the oracle's single-set result (whole CSR)."""
+    nl = W.recipe_netlist(8, 400, 15, 24, shuffle=True)
+    k = 4
+    u = W.union_netlist(nl, k)
+    sts = [W.random_stimuli(60 + c, nl.num_inputs, 40, 900, xz=0.1) for c in range(k)]
+    off, tr, base = [np.zeros(1, np.int64)], [], 0
+    for st in sts:
+        off.append(st.offsets[1:] + base)
+        base += int(st.offsets[-1])
+        tr.append(st.trans)
+    with gls.Context(0) as c:
+        c.load(u)
+        c.gls_set_input_waveforms(u.num_inputs, np.concatenate(off), np.concatenate(tr).astype(np.uint64))
+        c.gls_simulate(950)
+        w = c.gls_get_waveforms()
+    for ci, st in enumerate(sts):
+        ref = oracle.simulate(nl.num_inputs, nl.gate_type, nl.fanin_offsets, nl.fanin_net, nl.pin_delay,
+                              st.offsets, st.trans, 950)
+        got = np.concatenate([w.trans[w.offsets[n]:w.offsets[n + 1]] for n in W.union_nets(nl, k, ci)])
+        assert np.array_equal(got, ref.trans)
