@@ -36,6 +36,7 @@ import torch  # noqa: E402
 from paper_2304_13398_b200 import workloads as W  # noqa: E402
 
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+WINDOWS = {}   # N = 1 time windows per launch (--windows; measured slower: off by default)
 C5_SETS = int(os.environ.get("GLS_BENCH_C5_SETS", "64"))   # BASELINE configs[4]: 64 independent stimulus sets
 # Functional multi-rank runs on ONE GPU (not measurements): GLS_BENCH_BACKEND=gloo stages the
 # collectives through host memory and GLS_BENCH_ONE_GPU=1 puts every rank on cuda:0 (NCCL
@@ -63,6 +64,9 @@ def parse():
     ap.add_argument("--arena-gb", type=float, default=0.0)
     ap.add_argument("--engine", type=int, default=0)
     ap.add_argument("--scheduler", type=int, default=0)
+    ap.add_argument("--windows", type=int, default=0,
+                    help="N=1: time windows with the max-path-delay halo simulated as disjoint netlist "
+                         "copies in one launch (0: the config's default)")
     ap.add_argument("--c5-union", type=int, default=8,
                     help="C5: stimulus sets per launch (k disjoint netlist copies, one set each)")
     ap.add_argument("--ncycles", type=int, default=0,
@@ -340,7 +344,15 @@ def run_gls(a):
         UK = max(1, min(a.c5_union, len(sets)))
         while len(sets) % UK:
             UK -= 1
-    unl = W.union_netlist(nl, UK)
+    # N = 1 time windows (reading R17): the run split into KW windows with the max-path-delay
+    # halo, simulated as KW disjoint netlist copies in one launch — every copy's outputs are
+    # exact on its window, and a hot gate's work is split KW ways, which shortens the
+    # dependency chain through the hot cone that bounds C4
+    KW = 1
+    if not replicas and world == 1:
+        KW = a.windows if a.windows > 0 else WINDOWS.get(cfg, 1)
+    copies = UK if replicas else KW
+    unl = W.union_netlist(nl, copies)
     stream = torch.cuda.current_stream(dev)
     ctx = gls.Context(local, stream.cuda_stream)
     ctx.gls_set_config(chunk_events=a.chunk_events, blocks_per_sm=a.blocks_per_sm,
@@ -359,7 +371,30 @@ def run_gls(a):
     duration = plan["duration"]
     t = time.perf_counter()
     stims = []                       # this rank's given waveforms, resident in HBM: one per launch
-    for g0 in range(0, len(sets), UK):
+    halo_stim = None
+    if KW > 1:
+        offs, trs, hoffs, htrs, base, hbase = [], [], [], [], 0, 0
+        for k in range(KW):
+            pk = shard.rank_plan(k, KW, nc, H, spec.duration)
+            d_off, d_tr = W.window_stimuli(spec, *pk["gen_cycles"], dev)
+            offs.append(d_off if not offs else d_off[1:] + base)
+            base += int(d_tr.numel())
+            trs.append(d_tr)
+            # the same window's halo alone (cycles before its own): its evaluations are the
+            # ones the window repeats from its predecessor; counted once, then subtracted
+            k_lo = shard.time_window(k, KW, nc)[0]
+            if k == 0:
+                h_off, h_tr = torch.zeros(nl.num_inputs + 1, dtype=torch.int64, device=dev), d_tr[:0]
+            else:
+                h_off, h_tr = W.window_stimuli(spec, pk["gen_cycles"][0], k_lo, dev)
+            hoffs.append(h_off if not hoffs else h_off[1:] + hbase)
+            hbase += int(h_tr.numel())
+            htrs.append(h_tr)
+        stims.append((torch.cat(offs), torch.cat(trs), base))
+        halo_stim = (torch.cat(hoffs), torch.cat(htrs), hbase)
+        del offs, trs, hoffs, htrs
+        duration = spec.duration
+    for g0 in (range(0, len(sets), UK) if KW == 1 else []):
         offs, trs, base = [], [], 0
         for k in sets[g0:g0 + UK]:
             sp = W.config_stimspec(cfg, a.seed + k) if replicas else spec
@@ -374,7 +409,10 @@ def run_gls(a):
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()            # the generator's temporaries: leave the HBM to the library's arena
     d_off, d_tr, n_in = stims[0]
-    lens = (d_off[1:nl.num_inputs + 1] - d_off[:nl.num_inputs]).double()   # (set 0)
+    P_ = nl.num_inputs
+    lens = (d_off[1:P_ + 1] - d_off[:P_]).double()                              # (set 0)
+    for k in range(1, KW):                                                    # (windows: the whole run)
+        lens = lens + (d_off[k * P_ + 1:(k + 1) * P_ + 1] - d_off[k * P_:(k + 1) * P_]).double()
     wcv = float(lens.std(unbiased=False) / lens.mean()) if n_in else 0.0
     n_in_all = sum(x[2] for x in stims)
     log(f"stimuli: {len(stims)} set(s), {n_in_all} transitions on {spec.num_inputs} PIs, WCV {wcv:.2f} "
@@ -399,6 +437,15 @@ def run_gls(a):
             out.append(ctx.gls_get_stats())
         return out
 
+    halo_evals = halo_outs = 0
+    if halo_stim is not None:
+        ctx.gls_set_input_waveforms_device(unl.num_inputs, halo_stim[0].data_ptr(), halo_stim[1].data_ptr(), halo_stim[2])
+        ctx.gls_simulate(duration)
+        hs = ctx.gls_get_stats()
+        halo_evals, halo_outs = int(hs["gate_evals"]), int(hs["out_transitions"])
+        ctx.gls_set_input_waveforms_device(unl.num_inputs, d_off.data_ptr(), d_tr.data_ptr(), n_in)
+        log(f"{KW} windows: halo re-evaluations {halo_evals} gate-evals, {halo_outs} outputs (subtracted)")
+        del halo_stim
     for i in range(a.warmup):
         t = time.perf_counter()
         s = step()[0]
@@ -427,8 +474,8 @@ def run_gls(a):
     ck = clocks.stop()
     ms = ev0.elapsed_time(ev1) / a.steps
     s = st_[-1]
-    units = sum(x["gate_evals"] for x in st_)              # per step, this rank
-    outs = sum(x["out_transitions"] for x in st_)
+    units = sum(x["gate_evals"] for x in st_) - halo_evals  # per step, this rank (halo evaluations not counted)
+    outs = sum(x["out_transitions"] for x in st_) - halo_outs
     alg = statistics.mean(x["alg_bytes"] for x in st_)      # per kernel launch
     kms = statistics.mean(kernel_ms)                        # per kernel launch
     if world > 1:
@@ -481,7 +528,7 @@ def run_gls(a):
         e1.record(stream)
         torch.cuda.synchronize(dev)
         e_ms = e0.elapsed_time(e1) / n_e2e
-        e_units = sum(x["gate_evals"] for x in st_[:len(e_sets)])
+        e_units = sum(x["gate_evals"] for x in st_[:len(e_sets)]) - halo_evals
         if world > 1:
             import torch.distributed as dist
             tt = torch.tensor([e_ms, e_units], dtype=torch.float64, device=dev)
@@ -509,7 +556,7 @@ def run_gls(a):
             h_off.copy_(o_)
             h_tr.copy_(t_)
             t_hi = duration // 32
-            nn = nl.num_nets
+            nn = unl.num_nets
             d_o = torch.empty(nn + 1, dtype=torch.int64, device=dev)
             tot = ctx.gls_get_waveforms_range_device(0, nn, 0, t_hi, d_o.data_ptr())
             d_w = torch.empty(max(1, int(tot * 1.05) + 1024), dtype=torch.int64, device=dev)
@@ -521,7 +568,7 @@ def run_gls(a):
             w0.record(stream)
             d2h = 0
             for _ in range(n_e):
-                ctx.gls_set_input_waveforms(nl.num_inputs, h_off.numpy(), h_tr.numpy().view(np.uint64))
+                ctx.gls_set_input_waveforms(unl.num_inputs, h_off.numpy(), h_tr.numpy().view(np.uint64))
                 ctx.gls_simulate(duration)
                 tot = ctx.gls_get_waveforms_range_device(0, nn, 0, t_hi, d_o.data_ptr(), d_w.data_ptr(), d_w.numel())
                 h_o.copy_(d_o, non_blocking=True)
@@ -572,7 +619,7 @@ def run_gls(a):
                "sample": f"{cfg} netlist ({nl.num_gates} gates), first {cyc} of {nc} clock cycles "
                          f"(t <= {tmax} ps): {r.gate_evals} gate-evals in {dt:.2f} s, single thread",
                **host_cpu()}
-        gh = ctx.gls_get_net_hashes_window(0, tmax)[W.union_nets(nl, UK, 0)]   # (set 0: copy 0)
+        gh = ctx.gls_get_net_hashes_window(0, tmax)[W.union_nets(nl, copies, 0)]   # (set 0 / window 0: copy 0)
         mism = int((gh != r.hashes).sum())
         parity = {"window_ps": [0, tmax], "nets": int(gh.size), "hash_mismatches": mism,
                   "bit_exact": mism == 0}
@@ -612,7 +659,10 @@ def run_gls(a):
                        "stimulus_wcv": round(wcv, 2), "halo_ps": H,
                        **({"stimulus_sets": C5_SETS, "sets_per_rank": len(sets), "sets_per_launch": UK,
                            "stimulus_transitions_per_rank": n_in_all} if replicas else {}),
+                       **({"time_windows": KW, "halo_gate_evals_subtracted": halo_evals} if KW > 1 else {}),
                        "parallelism": (f"stimulus sets round-robin over {world} rank(s), no exchange" if replicas else
+                                       f"{KW} time windows with the max-path-delay halo as disjoint netlist copies in one launch"
+                                       if KW > 1 else
                                        f"time-windows x{world}" if world > 1 else "single GPU"),
                        "cache": "working set (given + computed waveforms) >> 126 MB L2; no flush needed"},
             "output_transitions_per_s": outs / (ms / 1e3),
